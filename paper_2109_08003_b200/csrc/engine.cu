@@ -1,0 +1,932 @@
+// The translation engine: device-resident weights, a capacity-sized
+// workspace, the packed-varlen encoder, the CUDA-graph-captured incremental
+// decoder and the corpus-level scheduler.
+//
+// Reference path it replaces (pkg/src/fastnmt):
+//   store.random_model / assemble_weights (store.py:191-253, :539-572)
+//     -> fnmt_engine_set_tensor + finalize (pre-transposed, cast, uploaded once)
+//   model.encode (model.py:261-287)            -> Engine::encode
+//   model.init_cross_cache (model.py:290-305)  -> Engine::cross_kv
+//   model.decode_step (model.py:308-344)       -> Engine::run_step (graph node list)
+//   search.greedy_translate (search.py:58-86)  -> fused argmax epilogue + greedy_update kernel
+//   batching.plan_batches / restore_order (batching.py:68-122)
+//                                              -> plan_batches (host) + scatter kernel
+//
+// Layout in HBM (compute dtype T = f16/bf16, or f32 in parity mode):
+//   weights: every projection W^T [N, K] (K-major), encoder/decoder q|k|v
+//   fused to [3d, d], cross k|v fused to [2d, d]; the vocab projection is the
+//   [V, d] embedding table itself (out_proj = src_embed^T => W^T = src_embed);
+//   fp32 copies of the lookup tables and the sinusoid table.
+//   encoder activations: packed varlen rows [tokens, *] (no padding rows).
+//   self K/V cache: per layer [rows * cap, d], row r's step j at r*cap + j.
+//   cross K/V: per layer packed [tokens, 2d].
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <numeric>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/fnmt_b200.h"
+#include "common.cuh"
+#include "engine.h"
+#include "kernels.h"
+
+namespace fnmt {
+
+namespace {
+
+__global__ void gather_batch_kernel(const int32_t* __restrict__ ids, const int64_t* __restrict__ off,
+                                    const int32_t* __restrict__ perm, const int32_t* __restrict__ cu,
+                                    int rows, int32_t* __restrict__ out_ids,
+                                    int32_t* __restrict__ out_pos) {
+  const int r = blockIdx.x;
+  if (r >= rows) return;
+  const int i = perm[r];
+  const int64_t src = off[i];
+  const int beg = cu[r], len = cu[r + 1] - cu[r];
+  for (int j = threadIdx.x; j < len; j += blockDim.x) {
+    out_ids[beg + j] = ids[src + j];
+    out_pos[beg + j] = j;
+  }
+}
+
+__global__ void scatter_out_kernel(const int32_t* __restrict__ out_ids, const int32_t* __restrict__ out_len,
+                                   int cap, const int32_t* __restrict__ perm, int rows,
+                                   const int64_t* __restrict__ dst_off, int32_t* __restrict__ dst_ids,
+                                   int32_t* __restrict__ dst_len) {
+  const int r = blockIdx.x;
+  if (r >= rows) return;
+  const int i = perm[r];
+  const int n = out_len[r];
+  const int64_t o = dst_off[i];
+  for (int j = threadIdx.x; j < n; j += blockDim.x) dst_ids[o + j] = out_ids[(size_t)r * cap + j];
+  if (threadIdx.x == 0) dst_len[i] = n;
+}
+
+__global__ void init_decode_kernel(int32_t* prev, uint8_t* finished, int32_t* out_len,
+                                   unsigned long long* keys, int32_t* t, int32_t* alive, int rows,
+                                   int bos) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
+    prev[r] = bos;
+    finished[r] = 0;
+    out_len[r] = 0;
+    keys[r] = 0ull;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *t = 0;
+    *alive = rows;
+  }
+}
+
+__global__ void fill_i32_kernel(int32_t* p, int n, int v) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = v;
+}
+
+__global__ void lens_from_cu_kernel(const int32_t* cu, int32_t* len, int R) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < R) len[r] = cu[r + 1] - cu[r];
+}
+
+__global__ void iota_pos_kernel(int32_t* pos, int b, int s) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < b * s) pos[i] = i % s;
+}
+
+__global__ void seq_table_kernel(int32_t* start, int32_t* qlen, int b, int s) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < b) {
+    start[i] = i * s;
+    qlen[i] = s;
+  }
+}
+
+}  // namespace
+
+thread_local std::string g_last_error;
+
+void set_error(const std::string& m) { g_last_error = m; }
+
+#define CK(expr)                                                                     \
+  do {                                                                               \
+    cudaError_t _e = (expr);                                                         \
+    if (_e != cudaSuccess) {                                                         \
+      throw EngineError(FNMT_E_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+    }                                                                                \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+
+std::vector<Batch> plan_batches(const std::vector<int32_t>& lengths, int sbatch, int wbatch) {
+  // batching.py:68-109: stable length-descending order, then greedy maximal
+  // batches under (count <= sbatch) and (count * longest <= wbatch).
+  std::vector<int32_t> order(lengths.size());
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int32_t a, int32_t b) { return lengths[a] > lengths[b]; });
+  std::vector<Batch> out;
+  Batch cur;
+  for (int32_t idx : order) {
+    const int32_t L = lengths[idx];
+    if (!cur.rows.empty()) {
+      const int64_t n1 = (int64_t)cur.rows.size() + 1;
+      if (n1 <= sbatch && n1 * cur.max_len <= wbatch) {
+        cur.rows.push_back(idx);
+        continue;
+      }
+      cur.oversize = cur.max_len > wbatch;
+      out.push_back(std::move(cur));
+      cur = Batch();
+    }
+    cur.rows.push_back(idx);
+    cur.max_len = L;
+  }
+  if (!cur.rows.empty()) {
+    cur.oversize = cur.max_len > wbatch;
+    out.push_back(std::move(cur));
+  }
+  return out;
+}
+
+int budget_of(int32_t len, float ratio, int offset, int max_positions) {
+  // search.py:49-51 (python float math: ceil(ratio * len) in double)
+  const double v = std::ceil((double)ratio * (double)len) + offset;
+  int64_t b = (int64_t)v;
+  b = std::min<int64_t>(b, max_positions);
+  return (int)std::max<int64_t>(1, b);
+}
+
+// ---------------------------------------------------------------------------
+
+Engine::Engine(const fnmt_arch& a, int device, int dtype) : arch(a), device(device), dt(dtype) {
+  if (a.n_enc_layers < 1 || a.n_dec_layers < 1 || a.d_model < 1 || a.n_heads_enc < 1 ||
+      a.n_heads_dec < 1 || a.ffn_dim_enc < 1 || a.vocab_size < 1 || a.max_positions < 1 ||
+      a.ffn_dim_dec < 0)
+    throw EngineError(FNMT_E_INVALID, "all sizes except ffn_dim_dec must be >= 1");
+  if (a.d_model % a.n_heads_enc || a.d_model % a.n_heads_dec)
+    throw EngineError(FNMT_E_INVALID, "d_model must be divisible by both head counts");
+  if (a.d_model % 8 || a.ffn_dim_enc % 8 || a.ffn_dim_dec % 8)
+    throw EngineError(FNMT_E_INVALID,
+                      "the B200 engine needs d_model and FFN widths divisible by 8 (TMA strides)");
+  if (dtype != kF32 && dtype != kF16 && dtype != kBF16)
+    throw EngineError(FNMT_E_INVALID, "dtype must be 0 (f32), 1 (f16) or 2 (bf16)");
+  CK(cudaSetDevice(device));
+  CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&ev_poll[0], cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&ev_poll[1], cudaEventDisableTiming));
+  CK(cudaEventCreate(&ev_t0));
+  CK(cudaEventCreate(&ev_t1));
+  CK(cudaHostAlloc(&h_alive, 4 * sizeof(int32_t), cudaHostAllocDefault));
+}
+
+Engine::~Engine() {
+  cudaSetDevice(device);
+  if (graph_exec) cudaGraphExecDestroy(graph_exec);
+  if (stream) cudaStreamSynchronize(stream);
+  for (void* p : allocations) cudaFree(p);
+  if (h_alive) cudaFreeHost(h_alive);
+  cudaEventDestroy(ev_poll[0]);
+  cudaEventDestroy(ev_poll[1]);
+  cudaEventDestroy(ev_t0);
+  cudaEventDestroy(ev_t1);
+  if (stream) cudaStreamDestroy(stream);
+}
+
+void* Engine::dalloc(size_t bytes) {
+  void* p = nullptr;
+  if (bytes == 0) bytes = 16;
+  CK(cudaMalloc(&p, bytes));
+  allocations.push_back(p);
+  device_bytes += (int64_t)bytes;
+  return p;
+}
+
+void Engine::set_tensor(const std::string& name, const float* host, int64_t numel) {
+  host_tensors[name].assign(host, host + numel);
+}
+
+const std::vector<float>& Engine::need(const std::string& name, int64_t numel) const {
+  auto it = host_tensors.find(name);
+  if (it == host_tensors.end()) throw EngineError(FNMT_E_INVALID, "missing tensor " + name);
+  if ((int64_t)it->second.size() != numel)
+    throw EngineError(FNMT_E_INVALID, "tensor " + name + " has " +
+                                          std::to_string(it->second.size()) + " values, expected " +
+                                          std::to_string(numel));
+  return it->second;
+}
+
+float* Engine::upload_f32(const std::vector<float>& v) {
+  float* p = (float*)dalloc(v.size() * sizeof(float));
+  CK(cudaMemcpy(p, v.data(), v.size() * sizeof(float), cudaMemcpyHostToDevice));
+  return p;
+}
+
+void* Engine::upload_act(const std::vector<float>& v) {
+  const size_t n = v.size();
+  if (dt == kF32) return upload_f32(v);
+  std::vector<uint16_t> h(n);
+  for (size_t i = 0; i < n; ++i) {
+    if (dt == kF16) {
+      __half x = __float2half_rn(v[i]);
+      std::memcpy(&h[i], &x, 2);
+    } else {
+      __nv_bfloat16 x = __float2bfloat16_rn(v[i]);
+      std::memcpy(&h[i], &x, 2);
+    }
+  }
+  void* p = dalloc(n * 2);
+  CK(cudaMemcpy(p, h.data(), n * 2, cudaMemcpyHostToDevice));
+  return p;
+}
+
+// Build W^T [sum(n_i), k] from reference-orientation weights [k, n_i] (x @ W).
+Lin Engine::make_lin(const std::vector<std::string>& wnames, const std::vector<std::string>& bnames,
+                     int k, const std::vector<int>& ns) {
+  int N = 0;
+  for (int n : ns) N += n;
+  std::vector<float> wt((size_t)N * k), bias(N);
+  int row0 = 0;
+  for (size_t p = 0; p < wnames.size(); ++p) {
+    const int n = ns[p];
+    const auto& w = need(wnames[p], (int64_t)k * n);
+    const auto& b = need(bnames[p], n);
+    for (int i = 0; i < k; ++i)
+      for (int j = 0; j < n; ++j) wt[(size_t)(row0 + j) * k + i] = w[(size_t)i * n + j];
+    std::copy(b.begin(), b.end(), bias.begin() + row0);
+    row0 += n;
+  }
+  Lin L;
+  L.N = N;
+  L.K = k;
+  L.w = upload_act(wt);
+  L.b = upload_f32(bias);
+  finish_lin(L);
+  return L;
+}
+
+void Engine::finish_lin(Lin& L) {
+  if (dt == kF32) return;
+  std::string err;
+  if (!make_tmap_16(&L.tm, L.w, dt, L.N, L.K, L.K, gemm_tile_n(), &err))
+    throw EngineError(FNMT_E_CUDA, "weight TMA descriptor: " + err);
+}
+
+Norm Engine::make_norm(const std::string& prefix) {
+  const int d = arch.d_model;
+  return Norm{upload_f32(need(prefix + ".gain", d)), upload_f32(need(prefix + ".bias", d))};
+}
+
+void Engine::finalize() {
+  CK(cudaSetDevice(device));
+  const int d = arch.d_model, V = arch.vocab_size;
+  const auto& src = need("src_embed", (int64_t)V * d);
+  src_emb32 = upload_f32(src);
+  if (arch.shared_embeddings) {
+    tgt_emb32 = src_emb32;
+  } else {
+    tgt_emb32 = upload_f32(need("tgt_embed", (int64_t)V * d));
+  }
+  // positions: prefer the caller's table (bit-identical to numpy's sinusoid);
+  // otherwise compute it (model.py:184-190).
+  if (host_tensors.count("positions")) {
+    pos32 = upload_f32(need("positions", (int64_t)arch.max_positions * d));
+  } else {
+    std::vector<float> p((size_t)arch.max_positions * d);
+    for (int r = 0; r < arch.max_positions; ++r)
+      for (int i = 0; i < d; ++i) {
+        const double ang = (double)r / std::pow(10000.0, (2.0 * std::floor(i / 2.0)) / d);
+        p[(size_t)r * d + i] = (float)((i % 2 == 0) ? std::sin(ang) : std::cos(ang));
+      }
+    pos32 = upload_f32(p);
+  }
+  // vocab projection W^T == out_proj table [V, d]
+  {
+    const std::vector<float>* table = &src;
+    if (!arch.shared_embeddings) table = &need("out_proj", (int64_t)V * d);
+    out.N = V;
+    out.K = d;
+    out.w = upload_act(*table);
+    out.b = upload_f32(need("out_bias", V));
+    finish_lin(out);
+  }
+  enc.clear();
+  for (int i = 0; i < arch.n_enc_layers; ++i) {
+    const std::string p = "enc." + std::to_string(i);
+    EncL L;
+    L.qkv = make_lin({p + ".attn.q_w", p + ".attn.k_w", p + ".attn.v_w"},
+                     {p + ".attn.q_b", p + ".attn.k_b", p + ".attn.v_b"}, d, {d, d, d});
+    L.o = make_lin({p + ".attn.o_w"}, {p + ".attn.o_b"}, d, {d});
+    L.f1 = make_lin({p + ".ffn.w1"}, {p + ".ffn.b1"}, d, {arch.ffn_dim_enc});
+    L.f2 = make_lin({p + ".ffn.w2"}, {p + ".ffn.b2"}, arch.ffn_dim_enc, {d});
+    L.n1 = make_norm(p + ".norm1");
+    L.n2 = make_norm(p + ".norm2");
+    enc.push_back(L);
+  }
+  dec.clear();
+  for (int i = 0; i < arch.n_dec_layers; ++i) {
+    const std::string p = "dec." + std::to_string(i);
+    DecL L;
+    L.sqkv = make_lin({p + ".self.q_w", p + ".self.k_w", p + ".self.v_w"},
+                      {p + ".self.q_b", p + ".self.k_b", p + ".self.v_b"}, d, {d, d, d});
+    L.so = make_lin({p + ".self.o_w"}, {p + ".self.o_b"}, d, {d});
+    L.cq = make_lin({p + ".cross.q_w"}, {p + ".cross.q_b"}, d, {d});
+    L.ckv = make_lin({p + ".cross.k_w", p + ".cross.v_w"}, {p + ".cross.k_b", p + ".cross.v_b"},
+                     d, {d, d});
+    L.co = make_lin({p + ".cross.o_w"}, {p + ".cross.o_b"}, d, {d});
+    L.n1 = make_norm(p + ".norm1");
+    L.n2 = make_norm(p + ".norm2");
+    L.ffn = arch.ffn_dim_dec > 0;
+    if (L.ffn) {
+      L.f1 = make_lin({p + ".ffn.w1"}, {p + ".ffn.b1"}, d, {arch.ffn_dim_dec});
+      L.f2 = make_lin({p + ".ffn.w2"}, {p + ".ffn.b2"}, arch.ffn_dim_dec, {d});
+      L.n3 = make_norm(p + ".norm3");
+    }
+    dec.push_back(L);
+  }
+  host_tensors.clear();
+  host_tensors.rehash(0);
+  finalized = true;
+  CK(cudaDeviceSynchronize());
+}
+
+// ---------------------------------------------------------------------------
+// workspace
+
+void Engine::reserve(int tok_cap, int row_cap, int64_t pool_cap) {
+  if (!finalized) throw EngineError(FNMT_E_STATE, "finalize() before reserve()");
+  if (tok_cap <= ws.tok_cap && row_cap <= ws.row_cap && pool_cap <= ws.pool_cap) return;
+  tok_cap = std::max(tok_cap, ws.tok_cap);
+  row_cap = std::max(row_cap, ws.row_cap);
+  pool_cap = std::max(pool_cap, ws.pool_cap);
+  CK(cudaStreamSynchronize(stream));
+  for (void* p : ws.owned) {
+    cudaFree(p);
+    allocations.erase(std::find(allocations.begin(), allocations.end(), p));
+  }
+  device_bytes -= ws.bytes;
+  ws = Workspace();
+  const int64_t before = device_bytes;
+  auto alloc = [&](size_t bytes) {
+    void* p = dalloc(bytes);
+    ws.owned.push_back(p);
+    return p;
+  };
+  const int d = arch.d_model, es = dtype_size(dt);
+  const int fe = arch.ffn_dim_enc, fd = std::max(arch.ffn_dim_dec, 1);
+  ws.tok_cap = tok_cap;
+  ws.row_cap = row_cap;
+  ws.pool_cap = pool_cap;
+  ws.ids = (int32_t*)alloc(sizeof(int32_t) * tok_cap);
+  ws.pos = (int32_t*)alloc(sizeof(int32_t) * tok_cap);
+  ws.cu = (int32_t*)alloc(sizeof(int32_t) * (row_cap + 1));
+  ws.len = (int32_t*)alloc(sizeof(int32_t) * row_cap);
+  ws.qstart = (int32_t*)alloc(sizeof(int32_t) * row_cap);
+  ws.qlen = (int32_t*)alloc(sizeof(int32_t) * row_cap);
+  ws.x32 = (float*)alloc(sizeof(float) * (size_t)tok_cap * d);
+  ws.y32 = (float*)alloc(sizeof(float) * (size_t)tok_cap * d);
+  ws.xa = dt == kF32 ? (void*)ws.x32 : alloc((size_t)es * tok_cap * d);
+  ws.qkv = alloc((size_t)es * tok_cap * 3 * d);
+  ws.att = alloc((size_t)es * tok_cap * d);
+  ws.h = alloc((size_t)es * tok_cap * fe);
+  ws.ckv.assign(arch.n_dec_layers, nullptr);
+  ws.kc.assign(arch.n_dec_layers, nullptr);
+  ws.vc.assign(arch.n_dec_layers, nullptr);
+  for (int l = 0; l < arch.n_dec_layers; ++l) {
+    ws.ckv[l] = alloc((size_t)es * tok_cap * 2 * d);
+    ws.kc[l] = alloc((size_t)es * pool_cap * d);
+    ws.vc[l] = alloc((size_t)es * pool_cap * d);
+  }
+  ws.dx32 = (float*)alloc(sizeof(float) * (size_t)row_cap * d);
+  ws.dy32 = (float*)alloc(sizeof(float) * (size_t)row_cap * d);
+  ws.dxa = dt == kF32 ? (void*)ws.dx32 : alloc((size_t)es * row_cap * d);
+  ws.dqkv = alloc((size_t)es * row_cap * 3 * d);
+  ws.datt = alloc((size_t)es * row_cap * d);
+  ws.dq = alloc((size_t)es * row_cap * d);
+  ws.dh = alloc((size_t)es * row_cap * fd);
+  ws.keys = (unsigned long long*)alloc(sizeof(unsigned long long) * row_cap);
+  ws.prev = (int32_t*)alloc(sizeof(int32_t) * row_cap);
+  ws.budget = (int32_t*)alloc(sizeof(int32_t) * row_cap);
+  ws.out_len = (int32_t*)alloc(sizeof(int32_t) * row_cap);
+  ws.finished = (uint8_t*)alloc(row_cap);
+  ws.out_ids = (int32_t*)alloc(sizeof(int32_t) * pool_cap);
+  ws.t = (int32_t*)alloc(sizeof(int32_t) * 4);
+  ws.alive = ws.t + 1;
+  if (dt != kF32) {
+    std::string err;
+    bool ok = make_tmap_16(&ws.tm_xa, ws.xa, dt, tok_cap, d, d, 128, &err) &&
+              make_tmap_16(&ws.tm_att, ws.att, dt, tok_cap, d, d, 128, &err) &&
+              make_tmap_16(&ws.tm_h, ws.h, dt, tok_cap, fe, fe, 128, &err) &&
+              make_tmap_16(&ws.tm_dxa, ws.dxa, dt, row_cap, d, d, 128, &err) &&
+              make_tmap_16(&ws.tm_datt, ws.datt, dt, row_cap, d, d, 128, &err) &&
+              make_tmap_16(&ws.tm_dh, ws.dh, dt, row_cap, fd, fd, 128, &err);
+    if (!ok) throw EngineError(FNMT_E_CUDA, "workspace TMA descriptor: " + err);
+  }
+  ws.bytes = device_bytes - before;
+}
+
+void Engine::reserve_for(const fnmt_run& run) {
+  const int tok = std::max(run.wbatch, arch.max_positions);
+  const int rows = std::max(run.sbatch, 1) * std::max(run.beam_size, 1);
+  const int64_t pool = std::max<int64_t>(
+      (int64_t)std::ceil(run.max_len_ratio * (double)run.wbatch) +
+          (int64_t)(run.max_len_offset + 1) * run.sbatch,
+      arch.max_positions) * std::max(run.beam_size, 1);
+  reserve(tok, rows, pool);
+}
+
+// ---------------------------------------------------------------------------
+// building blocks
+
+void Engine::gemm(const void* A, const CUtensorMap* tmA, int lda, const Lin& L, int M, void* C,
+                  int ldc, int c_dtype, int relu, cudaStream_t s) {
+  GemmArgs g;
+  g.A = A;
+  g.lda = lda;
+  g.W = L.w;
+  g.ldw = L.K;
+  g.in_dtype = dt;
+  g.bias = L.b;
+  g.M = M;
+  g.N = L.N;
+  g.K = L.K;
+  g.C = C;
+  g.ldc = ldc;
+  g.c_dtype = c_dtype;
+  g.relu = relu;
+  g.tmap_a = tmA;
+  g.tmap_w = dt == kF32 ? nullptr : &L.tm;
+  CK(launch_gemm(g, s));
+  ++launches;
+}
+
+void Engine::gemm_argmax(const void* A, const CUtensorMap* tmA, int lda, int M,
+                         unsigned long long* keys, cudaStream_t s) {
+  GemmArgs g;
+  g.A = A;
+  g.lda = lda;
+  g.W = out.w;
+  g.ldw = out.K;
+  g.in_dtype = dt;
+  g.bias = out.b;
+  g.M = M;
+  g.N = out.N;
+  g.K = out.K;
+  g.epi = kEpiArgmax;
+  g.keys = keys;
+  g.tmap_a = tmA;
+  g.tmap_w = dt == kF32 ? nullptr : &out.tm;
+  CK(launch_gemm(g, s));
+  ++launches;
+}
+
+void Engine::norm(const float* x, const float* y, const Norm& n, float* o32, void* oa, int rows,
+                  cudaStream_t s) {
+  CK(launch_add_norm(x, y, n.g, n.b, arch.norm_l1, o32, dt == kF32 ? nullptr : oa,
+                     dt, rows, arch.d_model, s));
+  ++launches;
+}
+
+// Encoder over rows already embedded in ws.x32 / ws.xa (model.py:279-286).
+void Engine::encoder_layers(int n_tok, int n_seq, int max_q, int max_k, const int32_t* qstart,
+                            const int32_t* qlen, const int32_t* kstart, const int32_t* klen,
+                            int k_pad, cudaStream_t s) {
+  const int d = arch.d_model;
+  const bool tc = dt != kF32;
+  for (const EncL& L : enc) {
+    gemm(ws.xa, tc ? &ws.tm_xa : nullptr, d, L.qkv, n_tok, ws.qkv, 3 * d, dt, 0, s);
+    AttnArgs a{};
+    a.q = ws.qkv;
+    a.ldq = 3 * d;
+    a.k = (const char*)ws.qkv + (size_t)d * dtype_size(dt);
+    a.v = (const char*)ws.qkv + (size_t)2 * d * dtype_size(dt);
+    a.ldkv = 3 * d;
+    a.out = ws.att;
+    a.ldo = d;
+    a.dtype = dt;
+    a.heads = arch.n_heads_enc;
+    a.dk = d / arch.n_heads_enc;
+    a.q_start = qstart;
+    a.q_len = qlen;
+    a.k_start = kstart;
+    a.k_len = klen;
+    a.k_pad = k_pad;
+    a.n_seq = n_seq;
+    a.max_q = max_q;
+    a.max_k = std::max(max_k, k_pad);
+    CK(launch_attention_varlen(a, s));
+    ++launches;
+    gemm(ws.att, tc ? &ws.tm_att : nullptr, d, L.o, n_tok, ws.y32, d, kF32, 0, s);
+    norm(ws.x32, ws.y32, L.n1, ws.x32, ws.xa, n_tok, s);
+    gemm(ws.xa, tc ? &ws.tm_xa : nullptr, d, L.f1, n_tok, ws.h, arch.ffn_dim_enc, dt, 1, s);
+    gemm(ws.h, tc ? &ws.tm_h : nullptr, arch.ffn_dim_enc, L.f2, n_tok, ws.y32, d, kF32, 0, s);
+    norm(ws.x32, ws.y32, L.n2, ws.x32, ws.xa, n_tok, s);
+  }
+}
+
+void Engine::cross_kv_all(int n_tok, cudaStream_t s) {
+  const int d = arch.d_model;
+  for (int l = 0; l < arch.n_dec_layers; ++l)
+    gemm(ws.xa, dt != kF32 ? &ws.tm_xa : nullptr, d, dec[l].ckv, n_tok, ws.ckv[l], 2 * d, dt, 0, s);
+}
+
+// One decoder step for v.rows rows (model.py:308-344).  All sizes that vary
+// per step live in device memory (step counter), so the launch sequence is
+// graph-capturable and replayable.
+void Engine::run_step(const StepView& v, cudaStream_t s) {
+  const int d = arch.d_model, es = dtype_size(dt);
+  const bool tc = dt != kF32;
+  const int R = v.rows;
+  CK(launch_embed(v.prev, nullptr, v.t_ptr, tgt_emb32, pos32, emb_scale(), ws.dx32,
+                  tc ? ws.dxa : nullptr, dt, R, d, s));
+  ++launches;
+  for (int l = 0; l < arch.n_dec_layers; ++l) {
+    const DecL& L = dec[l];
+    gemm(ws.dxa, tc ? &ws.tm_dxa : nullptr, d, L.sqkv, R, ws.dqkv, 3 * d, dt, 0, s);
+    DecAttnArgs a{};
+    a.q = ws.dqkv;
+    a.ldq = 3 * d;
+    a.k = v.kc[l];
+    a.v = v.vc[l];
+    a.ldkv = d;
+    a.k_w = v.kc[l];
+    a.v_w = v.vc[l];
+    a.new_k = (const char*)ws.dqkv + (size_t)d * es;
+    a.new_v = (const char*)ws.dqkv + (size_t)2 * d * es;
+    a.ld_new = 3 * d;
+    a.out = ws.datt;
+    a.ldo = d;
+    a.dtype = dt;
+    a.heads = arch.n_heads_dec;
+    a.dk = d / arch.n_heads_dec;
+    a.rows = R;
+    a.self_mode = 1;
+    a.cap = v.cap;
+    a.t_ptr = v.t_ptr;
+    a.anc = v.anc;
+    a.max_k = v.cap;
+    CK(launch_attention_decode(a, s));
+    ++launches;
+    gemm(ws.datt, tc ? &ws.tm_datt : nullptr, d, L.so, R, ws.dy32, d, kF32, 0, s);
+    norm(ws.dx32, ws.dy32, L.n1, ws.dx32, ws.dxa, R, s);
+    gemm(ws.dxa, tc ? &ws.tm_dxa : nullptr, d, L.cq, R, ws.dq, d, dt, 0, s);
+    DecAttnArgs c{};
+    c.q = ws.dq;
+    c.ldq = d;
+    c.k = v.ckv[l];
+    c.v = (const char*)v.ckv[l] + (size_t)d * es;
+    c.ldkv = 2 * d;
+    c.out = ws.datt;
+    c.ldo = d;
+    c.dtype = dt;
+    c.heads = arch.n_heads_dec;
+    c.dk = d / arch.n_heads_dec;
+    c.rows = R;
+    c.self_mode = 0;
+    c.k_start = v.k_start;
+    c.k_len = v.k_len;
+    c.k_pad = v.k_pad;
+    c.rows_per_seq = v.rows_per_seq;
+    c.max_k = v.max_k;
+    CK(launch_attention_decode(c, s));
+    ++launches;
+    gemm(ws.datt, tc ? &ws.tm_datt : nullptr, d, L.co, R, ws.dy32, d, kF32, 0, s);
+    norm(ws.dx32, ws.dy32, L.n2, ws.dx32, ws.dxa, R, s);
+    if (L.ffn) {
+      gemm(ws.dxa, tc ? &ws.tm_dxa : nullptr, d, L.f1, R, ws.dh, arch.ffn_dim_dec, dt, 1, s);
+      gemm(ws.dh, tc ? &ws.tm_dh : nullptr, arch.ffn_dim_dec, L.f2, R, ws.dy32, d, kF32, 0, s);
+      norm(ws.dx32, ws.dy32, L.n3, ws.dx32, ws.dxa, R, s);
+    }
+  }
+  if (v.logits) {
+    gemm(ws.dxa, tc ? &ws.tm_dxa : nullptr, d, out, R, v.logits, arch.vocab_size, kF32, 0, s);
+  } else {
+    gemm_argmax(ws.dxa, tc ? &ws.tm_dxa : nullptr, d, R, v.keys, s);
+  }
+}
+
+float Engine::emb_scale() const { return (float)std::sqrt((double)arch.d_model); }
+
+// ---------------------------------------------------------------------------
+// corpus translation
+
+void Engine::translate_device(const int32_t* d_ids, const int64_t* d_off,
+                              const std::vector<int32_t>& lengths, const fnmt_run& run,
+                              int32_t* d_out_ids, const int64_t* d_out_off, int32_t* d_out_len,
+                              fnmt_stats* st) {
+  if (!finalized) throw EngineError(FNMT_E_STATE, "engine not finalized");
+  if (run.beam_size != 1)
+    throw EngineError(FNMT_E_INVALID, "corpus translate: only greedy (beam_size 1) is implemented");
+  if (run.sbatch < 1 || run.wbatch < 1) throw EngineError(FNMT_E_INVALID, "sbatch/wbatch must be >= 1");
+  CK(cudaSetDevice(device));
+  const int n = (int)lengths.size();
+  for (int32_t L : lengths) {
+    if (L < 0) throw EngineError(FNMT_E_INVALID, "negative sentence length");
+    if (L > arch.max_positions)
+      throw EngineError(FNMT_E_LENGTH, "source length " + std::to_string(L) +
+                                           " exceeds max_positions " +
+                                           std::to_string(arch.max_positions));
+  }
+  const int64_t launches0 = launches;
+  CK(cudaEventRecord(ev_t0, stream));
+  // Empty sentences produce empty output without touching the GPU pipeline
+  // (the reference's Translator maps empty lines to empty lines).
+  std::vector<int32_t> live_len;
+  std::vector<int32_t> live_idx;
+  live_len.reserve(n);
+  live_idx.reserve(n);
+  for (int i = 0; i < n; ++i)
+    if (lengths[i] > 0) {
+      live_len.push_back(lengths[i]);
+      live_idx.push_back(i);
+    }
+  std::vector<Batch> plan = plan_batches(live_len, run.sbatch, run.wbatch);
+  // Host metadata for the whole plan: permutation (original sentence index
+  // per batch row), per-batch cu / budgets; uploaded once.
+  std::vector<int32_t> perm, cu_all, budget_all;
+  std::vector<int64_t> batch_row0, batch_cu0;
+  perm.reserve(live_idx.size());
+  for (const Batch& b : plan) {
+    batch_row0.push_back((int64_t)perm.size());
+    batch_cu0.push_back((int64_t)cu_all.size());
+    int32_t acc = 0;
+    for (int32_t li : b.rows) {
+      perm.push_back(live_idx[li]);
+      cu_all.push_back(acc);
+      acc += live_len[li];
+      budget_all.push_back(budget_of(live_len[li], run.max_len_ratio, run.max_len_offset,
+                                     arch.max_positions));
+    }
+    cu_all.push_back(acc);
+  }
+  // size the workspace for the largest batch of this plan (grows, never shrinks)
+  {
+    int tok_need = 1, rows_need = 1;
+    int64_t pool_need = 1;
+    for (size_t bi = 0; bi < plan.size(); ++bi) {
+      const int R = (int)plan[bi].rows.size();
+      const int n_tok = cu_all[batch_cu0[bi] + R];
+      int cap = 0;
+      for (int r = 0; r < R; ++r) cap = std::max(cap, budget_all[batch_row0[bi] + r]);
+      tok_need = std::max(tok_need, n_tok);
+      rows_need = std::max(rows_need, R);
+      pool_need = std::max<int64_t>(pool_need, (int64_t)R * cap);
+    }
+    reserve(tok_need, rows_need, pool_need);
+  }
+  ensure_meta(perm.size(), cu_all.size());
+  if (!perm.empty()) {
+    CK(cudaMemcpyAsync(meta_perm, perm.data(), perm.size() * 4, cudaMemcpyHostToDevice, stream));
+    CK(cudaMemcpyAsync(meta_cu, cu_all.data(), cu_all.size() * 4, cudaMemcpyHostToDevice, stream));
+    CK(cudaMemcpyAsync(meta_budget, budget_all.data(), budget_all.size() * 4,
+                       cudaMemcpyHostToDevice, stream));
+  }
+  // zero lengths for empty sentences
+  for (int i = 0; i < n; ++i)
+    if (lengths[i] == 0) {
+      // tiny synchronous-order write via the stream
+      CK(cudaMemsetAsync(d_out_len + i, 0, sizeof(int32_t), stream));
+    }
+  int64_t steps_total = 0, tgt_capacity = 0;
+  for (size_t bi = 0; bi < plan.size(); ++bi) {
+    const Batch& b = plan[bi];
+    const int R = (int)b.rows.size();
+    const int32_t* perm_b = meta_perm + batch_row0[bi];
+    const int32_t* cu_b = meta_cu + batch_cu0[bi];
+    int n_tok = 0, cap = 0;
+    for (int r = 0; r < R; ++r) {
+      n_tok += live_len[b.rows[r]];
+      cap = std::max(cap, budget_all[batch_row0[bi] + r]);
+    }
+    // 1) gather this batch's source ids into the packed workspace
+    gather_batch_kernel<<<R, 128, 0, stream>>>(d_ids, d_off, perm_b, cu_b, R, ws.ids, ws.pos);
+    CK(cudaGetLastError());
+    ++launches;
+    // per-sequence tables: q/k start = cu, len = cu diff
+    CK(cudaMemcpyAsync(ws.cu, cu_b, sizeof(int32_t) * (R + 1), cudaMemcpyDeviceToDevice, stream));
+    CK(cudaMemcpyAsync(ws.budget, meta_budget + batch_row0[bi], sizeof(int32_t) * R,
+                       cudaMemcpyDeviceToDevice, stream));
+    lens_from_cu(R);
+    // 2) encoder (packed varlen: only real tokens are rows)
+    CK(launch_embed(ws.ids, ws.pos, nullptr, src_emb32, pos32, emb_scale(), ws.x32,
+                    dt != kF32 ? ws.xa : nullptr, dt, n_tok, arch.d_model, stream));
+    ++launches;
+    encoder_layers(n_tok, R, b.max_len, b.max_len, ws.cu, ws.len, ws.cu, ws.len, 0, stream);
+    cross_kv_all(n_tok, stream);
+    // 3) greedy decode, one CUDA graph per step
+    init_decode_kernel<<<(R + 255) / 256, 256, 0, stream>>>(ws.prev, ws.finished, ws.out_len,
+                                                           ws.keys, ws.t, ws.alive, R, run.bos_id);
+    CK(cudaGetLastError());
+    ++launches;
+    StepView v;
+    v.rows = R;
+    v.cap = cap;
+    v.prev = ws.prev;
+    v.t_ptr = ws.t;
+    v.kc = ws.kc.data();
+    v.vc = ws.vc.data();
+    v.ckv = (const void* const*)ws.ckv.data();
+    v.k_start = ws.cu;
+    v.k_len = ws.len;
+    v.k_pad = 0;
+    v.rows_per_seq = 1;
+    v.max_k = b.max_len;
+    v.keys = ws.keys;
+    GreedyState gs;
+    gs.keys = ws.keys;
+    gs.prev = ws.prev;
+    gs.finished = ws.finished;
+    gs.budget = ws.budget;
+    gs.out_ids = ws.out_ids;
+    gs.out_len = ws.out_len;
+    gs.t = ws.t;
+    gs.alive = ws.alive;
+    gs.rows = R;
+    gs.out_cap = cap;
+    gs.eos = run.eos_id;
+    gs.pad = run.pad_id;
+    const int64_t nodes = capture_step(v, gs);
+    const int chunk = 8;
+    int steps = 0;
+    int inflight = 0;
+    bool stop = false;
+    for (int c0 = 0; c0 < cap && !stop; c0 += chunk) {
+      const int c1 = std::min(cap, c0 + chunk);
+      for (int t = c0; t < c1; ++t) CK(cudaGraphLaunch(graph_exec, stream));
+      steps += c1 - c0;
+      launches += nodes * (c1 - c0);
+      const int slot = (c0 / chunk) & 1;
+      if (inflight == 2) {
+        // wait for the chunk before the previous one; stop when every row finished
+        CK(cudaEventSynchronize(ev_poll[slot]));
+        if (h_alive[slot] == 0) stop = true;
+        --inflight;
+      }
+      CK(cudaMemcpyAsync(h_alive + slot, ws.alive, sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
+      CK(cudaEventRecord(ev_poll[slot], stream));
+      ++inflight;
+    }
+    steps_total += steps;
+    // 4) restore order: scatter rows to their sentence slots
+    scatter_out_kernel<<<R, 64, 0, stream>>>(ws.out_ids, ws.out_len, cap, perm_b, R, d_out_off,
+                                            d_out_ids, d_out_len);
+    CK(cudaGetLastError());
+    ++launches;
+    tgt_capacity += n_tok;
+  }
+  CK(cudaEventRecord(ev_t1, stream));
+  CK(cudaStreamSynchronize(stream));
+  if (st) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ev_t0, ev_t1);
+    st->sentences += n;
+    int64_t src = 0;
+    for (int32_t L : lengths) src += L;
+    st->source_tokens += src;
+    st->batches += (int64_t)plan.size();
+    st->decode_steps += steps_total;
+    st->gpu_launches += launches - launches0;
+    st->total_ms += ms;
+    st->device_bytes = device_bytes;
+  }
+}
+
+void Engine::lens_from_cu(int R) {
+  lens_from_cu_kernel<<<(R + 255) / 256, 256, 0, stream>>>(ws.cu, ws.len, R);
+  CK(cudaGetLastError());
+  ++launches;
+}
+
+void Engine::ensure_meta(size_t rows, size_t cus) {
+  if (rows > meta_rows_cap) {
+    meta_perm = (int32_t*)dalloc(std::max<size_t>(rows, 1) * 4);
+    meta_budget = (int32_t*)dalloc(std::max<size_t>(rows, 1) * 4);
+    meta_rows_cap = rows;
+  }
+  if (cus > meta_cu_cap) {
+    meta_cu = (int32_t*)dalloc(std::max<size_t>(cus, 1) * 4);
+    meta_cu_cap = cus;
+  }
+}
+
+// Capture one decode step (+ greedy bookkeeping) into a graph; reuse the
+// executable graph through cudaGraphExecUpdate when the topology matches.
+int64_t Engine::capture_step(const StepView& v, const GreedyState& gs) {
+  const int64_t l0 = launches;
+  cudaGraph_t g = nullptr;
+  CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeRelaxed));
+  try {
+    run_step(v, stream);
+    CK(launch_greedy_update(gs, stream));
+    ++launches;
+  } catch (...) {
+    cudaStreamEndCapture(stream, &g);
+    if (g) cudaGraphDestroy(g);
+    throw;
+  }
+  CK(cudaStreamEndCapture(stream, &g));
+  const int64_t nodes = launches - l0;
+  launches = l0;  // counted per replay by the caller
+  bool updated = false;
+  if (graph_exec) {
+    cudaGraphExecUpdateResultInfo info;
+    if (cudaGraphExecUpdate(graph_exec, g, &info) == cudaSuccess) updated = true;
+    else {
+      cudaGetLastError();
+      cudaGraphExecDestroy(graph_exec);
+      graph_exec = nullptr;
+    }
+  }
+  if (!updated) CK(cudaGraphInstantiate(&graph_exec, g, 0));
+  CK(cudaGraphDestroy(g));
+  return nodes;
+}
+
+// ---------------------------------------------------------------------------
+// protocol-level entry points (used by the Python drop-in TranslationModel)
+
+void Engine::encode_padded(const int32_t* d_tokens, const int32_t* d_lengths, int b, int s,
+                           float* d_states32, void* d_states_act) {
+  if (s > arch.max_positions)
+    throw EngineError(FNMT_E_LENGTH, "source length " + std::to_string(s) +
+                                         " exceeds max_positions " +
+                                         std::to_string(arch.max_positions));
+  const int n_tok = b * s;
+  if (n_tok == 0) return;
+  reserve(std::max(n_tok, ws.tok_cap), std::max(b, ws.row_cap), ws.pool_cap);
+  CK(cudaMemcpyAsync(ws.ids, d_tokens, sizeof(int32_t) * n_tok, cudaMemcpyDeviceToDevice, stream));
+  iota_pos_kernel<<<(n_tok + 255) / 256, 256, 0, stream>>>(ws.pos, b, s);
+  seq_table_kernel<<<(b + 255) / 256, 256, 0, stream>>>(ws.qstart, ws.qlen, b, s);
+  CK(cudaMemcpyAsync(ws.len, d_lengths, sizeof(int32_t) * b, cudaMemcpyDeviceToDevice, stream));
+  CK(launch_embed(ws.ids, ws.pos, nullptr, src_emb32, pos32, emb_scale(), ws.x32,
+                  dt != kF32 ? ws.xa : nullptr, dt, n_tok, arch.d_model, stream));
+  // queries: every padded position; keys: the real prefix (k_len 0 => all s masked)
+  encoder_layers(n_tok, b, s, s, ws.qstart, ws.qlen, ws.qstart, ws.len, s, stream);
+  if (d_states32)
+    CK(cudaMemcpyAsync(d_states32, ws.x32, sizeof(float) * n_tok * arch.d_model,
+                       cudaMemcpyDeviceToDevice, stream));
+  if (d_states_act)
+    CK(cudaMemcpyAsync(d_states_act, ws.xa, (size_t)dtype_size(dt) * n_tok * arch.d_model,
+                       cudaMemcpyDeviceToDevice, stream));
+  CK(cudaStreamSynchronize(stream));
+}
+
+void Engine::cross_kv(const void* d_states_act, int rows, int layer, void* d_out) {
+  if (layer < 0 || layer >= arch.n_dec_layers) throw EngineError(FNMT_E_INVALID, "bad layer");
+  GemmArgs g;
+  g.A = d_states_act;
+  g.lda = arch.d_model;
+  g.W = dec[layer].ckv.w;
+  g.ldw = dec[layer].ckv.K;
+  g.in_dtype = dt;
+  g.bias = dec[layer].ckv.b;
+  g.M = rows;
+  g.N = dec[layer].ckv.N;
+  g.K = dec[layer].ckv.K;
+  g.C = d_out;
+  g.ldc = 2 * arch.d_model;
+  g.c_dtype = dt;
+  g.tmap_w = dt == kF32 ? nullptr : &dec[layer].ckv.tm;
+  CK(launch_gemm(g, stream));
+  CK(cudaStreamSynchronize(stream));
+}
+
+void Engine::decode_step(const int32_t* d_prev, int t, int rows, int cap, void* const* self_k,
+                         void* const* self_v, const void* const* cross_kv,
+                         const int32_t* d_k_start, const int32_t* d_k_len, int k_pad, int max_k,
+                         float* d_logits) {
+  if (t >= arch.max_positions)
+    throw EngineError(FNMT_E_LENGTH, "decode position " + std::to_string(t) +
+                                         " exceeds max_positions " +
+                                         std::to_string(arch.max_positions));
+  if (t >= cap) throw EngineError(FNMT_E_INVALID, "self-attention cache capacity exceeded");
+  if (rows == 0) return;
+  reserve(ws.tok_cap, std::max(rows, ws.row_cap), ws.pool_cap);
+  fill_i32_kernel<<<1, 32, 0, stream>>>(ws.t, 1, t);
+  CK(cudaMemcpyAsync(ws.prev, d_prev, sizeof(int32_t) * rows, cudaMemcpyDeviceToDevice, stream));
+  StepView v;
+  v.rows = rows;
+  v.cap = cap;
+  v.prev = ws.prev;
+  v.t_ptr = ws.t;
+  std::vector<void*> kc(self_k, self_k + arch.n_dec_layers), vc(self_v, self_v + arch.n_dec_layers);
+  std::vector<const void*> ckv(cross_kv, cross_kv + arch.n_dec_layers);
+  v.kc = kc.data();
+  v.vc = vc.data();
+  v.ckv = ckv.data();
+  v.k_start = d_k_start;
+  v.k_len = d_k_len;
+  v.k_pad = k_pad;
+  v.rows_per_seq = 1;
+  v.max_k = std::max(max_k, k_pad);
+  v.logits = d_logits;
+  run_step(v, stream);
+  CK(cudaStreamSynchronize(stream));
+}
+
+}  // namespace fnmt

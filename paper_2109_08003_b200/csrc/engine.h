@@ -1,0 +1,162 @@
+// Engine object behind the fnmt_engine_* C ABI (see engine.cu).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/fnmt_b200.h"
+#include "kernels.h"
+
+namespace fnmt {
+
+struct EngineError {
+  int code;
+  std::string msg;
+  EngineError(int c, std::string m) : code(c), msg(std::move(m)) {}
+};
+
+extern thread_local std::string g_last_error;
+void set_error(const std::string& m);
+
+struct Lin {
+  void* w = nullptr;   // W^T [N, K] in the compute dtype
+  float* b = nullptr;  // [N]
+  int N = 0, K = 0;
+  CUtensorMap tm;      // TMA descriptor of W^T (tensor-core path)
+};
+struct Norm {
+  float* g = nullptr;
+  float* b = nullptr;
+};
+struct EncL {
+  Lin qkv, o, f1, f2;
+  Norm n1, n2;
+};
+struct DecL {
+  Lin sqkv, so, cq, ckv, co, f1, f2;
+  Norm n1, n2, n3;
+  bool ffn = false;
+};
+
+struct Batch {
+  std::vector<int32_t> rows;  // indices into the planned length list
+  int32_t max_len = 0;
+  bool oversize = false;
+};
+std::vector<Batch> plan_batches(const std::vector<int32_t>& lengths, int sbatch, int wbatch);
+int budget_of(int32_t len, float ratio, int offset, int max_positions);
+
+struct Workspace {
+  int tok_cap = 0, row_cap = 0;
+  int64_t pool_cap = 0;
+  int64_t bytes = 0;
+  std::vector<void*> owned;
+  int32_t *ids = nullptr, *pos = nullptr, *cu = nullptr, *len = nullptr;
+  int32_t *qstart = nullptr, *qlen = nullptr;
+  float *x32 = nullptr, *y32 = nullptr;
+  void *xa = nullptr, *qkv = nullptr, *att = nullptr, *h = nullptr;
+  std::vector<void*> ckv, kc, vc;
+  float *dx32 = nullptr, *dy32 = nullptr;
+  void *dxa = nullptr, *dqkv = nullptr, *datt = nullptr, *dq = nullptr, *dh = nullptr;
+  unsigned long long* keys = nullptr;
+  int32_t *prev = nullptr, *budget = nullptr, *out_len = nullptr, *out_ids = nullptr;
+  int32_t *t = nullptr, *alive = nullptr;
+  uint8_t* finished = nullptr;
+  CUtensorMap tm_xa, tm_att, tm_h, tm_dxa, tm_datt, tm_dh;
+};
+
+struct StepView {
+  int rows = 0, cap = 0;
+  const int32_t* prev = nullptr;
+  const int32_t* t_ptr = nullptr;
+  void* const* kc = nullptr;
+  void* const* vc = nullptr;
+  const void* const* ckv = nullptr;
+  const int32_t* k_start = nullptr;
+  const int32_t* k_len = nullptr;
+  int k_pad = 0, rows_per_seq = 1, max_k = 0;
+  const int32_t* anc = nullptr;
+  unsigned long long* keys = nullptr;  // argmax output (greedy)
+  float* logits = nullptr;             // or full logits (protocol path)
+};
+
+class Engine {
+ public:
+  Engine(const fnmt_arch& a, int device, int dtype);
+  ~Engine();
+
+  void set_tensor(const std::string& name, const float* host, int64_t numel);
+  void finalize();
+  void reserve(int tok_cap, int row_cap, int64_t pool_cap);
+  void reserve_for(const fnmt_run& run);
+
+  void translate_device(const int32_t* d_ids, const int64_t* d_off,
+                        const std::vector<int32_t>& lengths, const fnmt_run& run,
+                        int32_t* d_out_ids, const int64_t* d_out_off, int32_t* d_out_len,
+                        fnmt_stats* st);
+
+  void encode_padded(const int32_t* d_tokens, const int32_t* d_lengths, int b, int s,
+                     float* d_states32, void* d_states_act);
+  void cross_kv(const void* d_states_act, int rows, int layer, void* d_out);
+  void decode_step(const int32_t* d_prev, int t, int rows, int cap, void* const* self_k,
+                   void* const* self_v, const void* const* cross_kv, const int32_t* d_k_start,
+                   const int32_t* d_k_len, int k_pad, int max_k, float* d_logits);
+
+  fnmt_arch arch;
+  int device;
+  int dt;
+  cudaStream_t stream = nullptr;
+  int64_t device_bytes = 0;
+  int64_t launches = 0;
+
+ private:
+  void* dalloc(size_t bytes);
+  const std::vector<float>& need(const std::string& name, int64_t numel) const;
+  float* upload_f32(const std::vector<float>& v);
+  void* upload_act(const std::vector<float>& v);
+  Lin make_lin(const std::vector<std::string>& wnames, const std::vector<std::string>& bnames,
+               int k, const std::vector<int>& ns);
+  void finish_lin(Lin& L);
+  Norm make_norm(const std::string& prefix);
+  float emb_scale() const;
+
+  void gemm(const void* A, const CUtensorMap* tmA, int lda, const Lin& L, int M, void* C, int ldc,
+            int c_dtype, int relu, cudaStream_t s);
+  void gemm_argmax(const void* A, const CUtensorMap* tmA, int lda, int M,
+                   unsigned long long* keys, cudaStream_t s);
+  void norm(const float* x, const float* y, const Norm& n, float* o32, void* oa, int rows,
+            cudaStream_t s);
+  void encoder_layers(int n_tok, int n_seq, int max_q, int max_k, const int32_t* qstart,
+                      const int32_t* qlen, const int32_t* kstart, const int32_t* klen, int k_pad,
+                      cudaStream_t s);
+  void cross_kv_all(int n_tok, cudaStream_t s);
+  void run_step(const StepView& v, cudaStream_t s);
+  int64_t capture_step(const StepView& v, const GreedyState& gs);
+  void lens_from_cu(int R);
+  void ensure_meta(size_t rows, size_t cus);
+
+  std::unordered_map<std::string, std::vector<float>> host_tensors;
+  bool finalized = false;
+  std::vector<void*> allocations;
+  float* src_emb32 = nullptr;
+  float* tgt_emb32 = nullptr;
+  float* pos32 = nullptr;
+  Lin out;
+  std::vector<EncL> enc;
+  std::vector<DecL> dec;
+  Workspace ws;
+  cudaGraphExec_t graph_exec = nullptr;
+  cudaEvent_t ev_poll[2] = {nullptr, nullptr};
+  cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr;
+  int32_t* h_alive = nullptr;
+  int32_t* meta_perm = nullptr;
+  int32_t* meta_cu = nullptr;
+  int32_t* meta_budget = nullptr;
+  size_t meta_rows_cap = 0, meta_cu_cap = 0;
+};
+
+}  // namespace fnmt

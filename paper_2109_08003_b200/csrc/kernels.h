@@ -1,0 +1,129 @@
+// Internal launcher declarations shared by the engine and the C-ABI layer.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+namespace fnmt {
+
+// GEMM epilogues: what happens to acc = A[m,:] . W[n,:] (fp32) for each (m, n).
+enum Epilogue : int {
+  kEpiStore = 0,   // C[m,n] = act(acc + bias[n] (+ resid[m,n]))   in c_dtype
+  kEpiArgmax = 1,  // keys[m] = max over n < valid_n of key(acc + bias[n], n)
+};
+
+struct GemmArgs {
+  const void* A = nullptr;  // [M, K] row-major, leading dim lda (elements)
+  int lda = 0;
+  const void* W = nullptr;  // [N, K] row-major (K-major), leading dim ldw
+  int ldw = 0;
+  int in_dtype = 1;         // kF32 -> SIMT fp32 path; kF16 / kBF16 -> tcgen05 path
+  const float* bias = nullptr;
+  int M = 0, N = 0, K = 0;
+  int epi = kEpiStore;
+  void* C = nullptr;
+  int ldc = 0;
+  int c_dtype = 0;
+  int relu = 0;
+  const float* resid = nullptr;  // optional fp32 residual added before store
+  int ld_resid = 0;
+  unsigned long long* keys = nullptr;  // argmax keys per row (must be pre-zeroed)
+  // Pre-encoded TMA descriptors (tcgen05 path).  If null the launcher encodes
+  // them on the fly (host cost ~ microseconds).
+  const CUtensorMap* tmap_a = nullptr;
+  const CUtensorMap* tmap_w = nullptr;
+};
+
+// Encode a 2-D TMA descriptor for a row-major [rows, cols] 16-bit matrix with
+// leading dimension ld (elements), box = [box_rows, 64 cols], 128 B swizzle.
+bool make_tmap_16(CUtensorMap* out, const void* base, int dtype, int64_t rows, int64_t cols,
+                  int64_t ld, int box_rows, std::string* err);
+
+int gemm_tile_n();  // N tile of the tcgen05 kernel (for W descriptors)
+
+cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t s);
+
+// ---------------------------------------------------------------------------
+// row kernels
+
+// x32[i,:] = table[ids[i],:] * scale + pos_table[pos(i),:]
+// pos(i) = pos_ids ? pos_ids[i] : (*pos_scalar)  (device step counter)
+cudaError_t launch_embed(const int32_t* ids, const int32_t* pos_ids, const int32_t* pos_scalar,
+                         const float* table, const float* pos_table, float scale, float* x32,
+                         void* xact, int act_dtype, int n, int d, cudaStream_t s);
+
+// out = norm(x + y) with gain/bias; variant 0 = l2, 1 = l1 (tensor.py:98-129)
+cudaError_t launch_add_norm(const float* x, const float* y, const float* gain,
+                            const float* bias, int l1, float* out32, void* out_act,
+                            int act_dtype, int rows, int d, cudaStream_t s);
+
+// ---------------------------------------------------------------------------
+// attention (model.py:199-240)
+
+struct AttnArgs {
+  const void* q; int ldq;         // query rows
+  const void* k; const void* v; int ldkv;  // key / value rows
+  void* out; int ldo;
+  int dtype;                      // storage dtype of q/k/v/out
+  int heads, dk;
+  // varlen description: sequence b has queries rows [q_start[b], q_start[b]+q_len[b])
+  // and keys rows [k_start[b], k_start[b] + k_len[b]); k_len[b]==0 means "all
+  // k_pad keys masked" (reference's -1e9 everywhere case).
+  const int32_t* q_start; const int32_t* q_len;
+  const int32_t* k_start; const int32_t* k_len;
+  int k_pad;                      // padded key count for the all-masked case
+  int n_seq, max_q, max_k;
+};
+cudaError_t launch_attention_varlen(const AttnArgs& a, cudaStream_t s);
+
+// Single-query attention for the incremental decoder.
+// Self mode: keys of row r live at kv + (r*cap + j)*ldkv, j in [0, len) where
+//   len = *len_scalar + 1 (device step counter), and this step's k/v (from
+//   new_k/new_v rows) is first written to slot j = *len_scalar.
+//   anc (optional, beam): key j of row r is taken from cache row anc[r*cap + j].
+// Cross mode: row r attends to sequence seq = r / rows_per_seq, keys
+//   kv + (k_start[seq] + j)*ldkv for j < k_len[seq] (k_len 0 -> all k_pad masked).
+struct DecAttnArgs {
+  const void* q; int ldq;
+  const void* k; const void* v; int ldkv;
+  void* k_w; void* v_w;                 // self mode: caches written at slot t
+  const void* new_k; const void* new_v; int ld_new;
+  void* out; int ldo;
+  int dtype, heads, dk, rows;
+  int self_mode;
+  int cap;                              // self: slots per row
+  const int32_t* t_ptr;                 // self: device step counter
+  const int32_t* anc;                   // self beam: ancestor table [rows, cap] or null
+  const int32_t* k_start; const int32_t* k_len; int k_pad; int rows_per_seq;
+  int max_k;
+};
+cudaError_t launch_attention_decode(const DecAttnArgs& a, cudaStream_t s);
+
+// ---------------------------------------------------------------------------
+// search bookkeeping (search.py:58-86)
+
+struct GreedyState {
+  unsigned long long* keys;   // [rows] argmax keys of this step (reset to 0 here)
+  int32_t* prev;              // [rows] next decoder input
+  uint8_t* finished;          // [rows]
+  const int32_t* budget;      // [rows]
+  int32_t* out_ids;           // [rows, out_cap]
+  int32_t* out_len;           // [rows]
+  int32_t* t;                 // device step counter (incremented here)
+  int32_t* alive;             // [1] rows still running after this step
+  int rows, out_cap, eos, pad;
+};
+cudaError_t launch_greedy_update(const GreedyState& g, cudaStream_t s);
+
+cudaError_t launch_keys_to_index(const unsigned long long* keys, int rows, int32_t* out,
+                                 cudaStream_t s);
+cudaError_t launch_argmax_rows(const float* logits, int ld, int rows, int n,
+                               int32_t* out_idx, cudaStream_t s);
+cudaError_t launch_gather_rows(const void* src, void* dst, const int32_t* idx, int rows,
+                               int64_t row_bytes, int64_t src_stride, int64_t dst_stride,
+                               cudaStream_t s);
+
+}  // namespace fnmt

@@ -1,0 +1,151 @@
+"""Corpus-level translation on the B200 engine.
+
+``Engine`` wraps one ``fnmt_engine`` per GPU and exposes the reference's
+batch-translate contract at the id level: length-sorted token-budget
+batching (batching.py:100-109), greedy decode of every batch
+(search.py:58-86) and order restoration (batching.py:112-122) — all inside
+one native call.  Two entry points, matching the two halves of the bench:
+
+* :meth:`Engine.translate` — host (numpy / pinned torch) buffers in and out;
+  the host<->device copies happen inside the call (the ``e2e`` path);
+* :meth:`Engine.translate_device` — inputs and outputs already in HBM.
+
+``RunConfig`` mirrors the reference's run flags (cli.py:20-45) with the GPU
+decoding caps of the paper (sbatch 3072 / wbatch 64000).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _capi
+from ._capi import check, lib, ptr
+from .store import BOS_ID, EOS_ID, PAD_ID
+
+
+@dataclass(frozen=True)
+class RunConfig:
+    precision: str = "f16"          # f16 / bf16 / f32 (parity mode)
+    sbatch: int = 3072
+    wbatch: int = 64000
+    workers: int = 1                # GPUs (one process each; see bench.py)
+    chunk_lines: int = 2000
+    beam: int = 1
+    pretokenized: bool = False
+    max_len_ratio: float = 1.5
+    max_len_offset: int = 5
+
+
+def run_struct(sbatch, wbatch, ratio=1.5, offset=5, beam=1, bos=BOS_ID, eos=EOS_ID,
+               pad=PAD_ID) -> _capi.fnmt_run:
+    return _capi.fnmt_run(int(sbatch), int(wbatch), float(ratio), int(offset), int(beam),
+                          int(bos), int(eos), int(pad))
+
+
+def budgets_of(lengths: np.ndarray, ratio: float, offset: int, max_positions: int) -> np.ndarray:
+    lengths = np.ascontiguousarray(lengths, dtype=np.int32)
+    out = np.empty_like(lengths)
+    check(lib.fnmt_budgets(lengths.ctypes.data, len(lengths), float(ratio), int(offset),
+                           int(max_positions), out.ctypes.data), "budgets")
+    return out
+
+
+def stats_dict(st: _capi.fnmt_stats) -> dict:
+    return {name: getattr(st, name) for name, _ in st._fields_}
+
+
+class Engine:
+    """Native corpus translator on one GPU."""
+
+    def __init__(self, cfg, weights, dtype: str = "f16", device: int = 0):
+        from .model import EngineHandle
+        self.handle = weights if isinstance(weights, EngineHandle) else EngineHandle(
+            cfg, weights, dtype=dtype, device=device)
+        self.cfg = self.handle.cfg
+
+    def reserve(self, sbatch=3072, wbatch=64000, ratio=1.5, offset=5):
+        r = run_struct(sbatch, wbatch, ratio, offset)
+        check(lib.fnmt_engine_reserve(self.handle.h, C.byref(r)), "reserve")
+
+    def plan_outputs(self, lengths, ratio=1.5, offset=5):
+        b = budgets_of(lengths, ratio, offset, self.cfg.max_positions)
+        off = np.zeros(len(b), dtype=np.int64)
+        if len(b):
+            np.cumsum(b[:-1], out=off[1:])
+        return b, off
+
+    def translate(self, ids: np.ndarray, offsets: np.ndarray, sbatch=3072, wbatch=64000,
+                  ratio=1.5, offset=5, out_ids=None, out_len=None, out_off=None):
+        """Host buffers.  ids int32 (flat), offsets int64 [n+1].  Returns
+        (out_ids flat int32 laid out at out_off, out_len int32 [n], out_off, stats)."""
+        ids = np.ascontiguousarray(ids, dtype=np.int32) if isinstance(ids, np.ndarray) else ids
+        offsets = np.ascontiguousarray(offsets, dtype=np.int64) if isinstance(
+            offsets, np.ndarray) else offsets
+        n = len(offsets) - 1
+        lengths = np.diff(np.asarray(offsets)).astype(np.int32)
+        if out_off is None:
+            b, out_off = self.plan_outputs(lengths, ratio, offset)
+            total = int(b.sum())
+        else:
+            total = None
+        if out_ids is None:
+            out_ids = np.empty(max(total or 0, 1), dtype=np.int32)
+        if out_len is None:
+            out_len = np.empty(max(n, 1), dtype=np.int32)
+        st = _capi.fnmt_stats()
+        r = run_struct(sbatch, wbatch, ratio, offset)
+        check(lib.fnmt_engine_translate(self.handle.h, ptr(ids), ptr(offsets), n, C.byref(r),
+                                        ptr(out_ids), ptr(out_off), ptr(out_len), C.byref(st)),
+              "translate")
+        return out_ids, out_len, out_off, st
+
+    def translate_device(self, d_ids: torch.Tensor, d_offsets: torch.Tensor, lengths: np.ndarray,
+                         d_out_ids: torch.Tensor, out_off: np.ndarray, d_out_off: torch.Tensor,
+                         d_out_len: torch.Tensor, sbatch=3072, wbatch=64000, ratio=1.5, offset=5):
+        lengths = np.ascontiguousarray(lengths, dtype=np.int32)
+        st = _capi.fnmt_stats()
+        r = run_struct(sbatch, wbatch, ratio, offset)
+        check(lib.fnmt_engine_translate_device(
+            self.handle.h, ptr(d_ids), ptr(d_offsets), lengths.ctypes.data, len(lengths),
+            C.byref(r), ptr(d_out_ids), out_off.ctypes.data, ptr(d_out_off), ptr(d_out_len),
+            C.byref(st)), "translate_device")
+        return st
+
+    def device_bytes(self) -> int:
+        return self.handle.device_bytes()
+
+
+def translate_ids(handle, rows, search=None, sbatch=3072, wbatch=64000) -> list[list[int]]:
+    """Greedy-translate a list of id sequences through the native corpus path."""
+    ratio = getattr(search, "max_len_ratio", 1.5)
+    offset = getattr(search, "max_len_offset", 5)
+    bos = getattr(search, "bos_id", BOS_ID)
+    eos = getattr(search, "eos_id", EOS_ID)
+    pad = getattr(search, "pad_id", PAD_ID)
+    rows = [np.asarray(r, dtype=np.int64) for r in rows]
+    n = len(rows)
+    if n == 0:
+        return []
+    lengths = np.array([len(r) for r in rows], dtype=np.int32)
+    offsets = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(lengths, out=offsets[1:])
+    ids = np.concatenate(rows).astype(np.int32) if offsets[-1] else np.zeros(1, np.int32)
+    cfg = handle.cfg
+    if ids.size and offsets[-1] and (ids.min() < 0 or ids.max() >= cfg.vocab_size):
+        raise ValueError("token id out of range")
+    budgets = budgets_of(lengths, ratio, offset, cfg.max_positions)
+    out_off = np.zeros(n, dtype=np.int64)
+    np.cumsum(budgets[:-1], out=out_off[1:])
+    out_ids = np.empty(max(int(budgets.sum()), 1), dtype=np.int32)
+    out_len = np.empty(n, dtype=np.int32)
+    st = _capi.fnmt_stats()
+    r = run_struct(sbatch, min(wbatch, int(lengths.max(initial=1)) * n), ratio, offset, 1, bos,
+                   eos, pad)
+    check(lib.fnmt_engine_translate(handle.h, ids.ctypes.data, offsets.ctypes.data, n,
+                                    C.byref(r), out_ids.ctypes.data, out_off.ctypes.data,
+                                    out_len.ctypes.data, C.byref(st)), "translate")
+    return [out_ids[o:o + L].tolist() for o, L in zip(out_off, out_len)]

@@ -177,6 +177,19 @@ int fnmt_engine_decode_step(fnmt_engine* e, const int32_t* d_prev, int t, int ro
 int64_t fnmt_engine_device_bytes(const fnmt_engine* e);
 void* fnmt_engine_stream(fnmt_engine* e);
 
+/* Kernel classes for the per-launch profiler. */
+enum {
+  FNMT_K_EMBED = 0, FNMT_K_GEMM_ENC, FNMT_K_ATTN_ENC, FNMT_K_NORM, FNMT_K_GEMM_DEC,
+  FNMT_K_ATTN_DEC, FNMT_K_VOCAB, FNMT_K_SEARCH, FNMT_K_OTHER, FNMT_K_COUNT
+};
+/* enable != 0: bracket every engine launch with CUDA events on the engine
+ * stream (decode steps run un-captured) and reset the counters. */
+int fnmt_engine_profile(fnmt_engine* e, int enable);
+/* Per-class totals (arrays of FNMT_K_COUNT): device ms, launches, algorithmic
+ * FLOPs, algorithmic bytes. */
+int fnmt_engine_profile_read(fnmt_engine* e, double* ms, int64_t* launches, double* flops,
+                             double* bytes);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

@@ -76,7 +76,12 @@ _SIGNATURES = {
                                      _VP]),
     "fnmt_engine_device_bytes": (_I64, [_VP]),
     "fnmt_engine_stream": (_VP, [_VP]),
+    "fnmt_engine_profile": (_I, [_VP, _I]),
+    "fnmt_engine_profile_read": (_I, [_VP, _VP, _VP, _VP, _VP]),
 }
+
+KERNEL_CLASSES = ("embed", "gemm_enc", "attn_enc", "norm", "gemm_dec", "attn_dec", "vocab_argmax",
+                  "search", "other")
 
 EXPORTED = tuple(_SIGNATURES)
 

@@ -354,6 +354,27 @@ int fnmt_engine_decode_step(fnmt_engine* e, const int32_t* d_prev, int t, int ro
   });
 }
 
+int fnmt_engine_profile(fnmt_engine* e, int enable) {
+  if (!e) return fail(FNMT_E_INVALID, "null engine");
+  return guarded([&] {
+    cudaSetDevice(e->eng->device);
+    e->eng->set_profiling(enable != 0);
+    return FNMT_OK;
+  });
+}
+
+int fnmt_engine_profile_read(fnmt_engine* e, double* ms, int64_t* launches, double* flops,
+                             double* bytes) {
+  if (!e) return fail(FNMT_E_INVALID, "null engine");
+  for (int i = 0; i < FNMT_K_COUNT; ++i) {
+    if (ms) ms[i] = e->eng->prof_ms[i];
+    if (launches) launches[i] = e->eng->prof_n[i];
+    if (flops) flops[i] = e->eng->prof_flops[i];
+    if (bytes) bytes[i] = e->eng->prof_bytes[i];
+  }
+  return FNMT_OK;
+}
+
 int64_t fnmt_engine_device_bytes(const fnmt_engine* e) { return e ? e->eng->device_bytes : 0; }
 
 void* fnmt_engine_stream(fnmt_engine* e) { return e ? (void*)e->eng->stream : nullptr; }

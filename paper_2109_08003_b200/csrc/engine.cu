@@ -185,7 +185,53 @@ Engine::Engine(const fnmt_arch& a, int device, int dtype) : arch(a), device(devi
   CK(cudaHostAlloc(&h_alive, 4 * sizeof(int32_t), cudaHostAllocDefault));
 }
 
+void Engine::set_profiling(bool on) {
+  CK(cudaStreamSynchronize(stream));
+  profiling = on;
+  prof_used = 0;
+  prof_recs.clear();
+  for (int i = 0; i < FNMT_K_COUNT; ++i) {
+    prof_ms[i] = prof_flops[i] = prof_bytes[i] = 0.0;
+    prof_n[i] = 0;
+  }
+}
+
+int Engine::prof_begin(cudaStream_t s) {
+  if (!profiling) return -1;
+  if (prof_used + 2 > prof_events.size()) {
+    for (int i = 0; i < 256; ++i) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      prof_events.push_back(e);
+    }
+  }
+  const int ev = (int)prof_used;
+  prof_used += 2;
+  CK(cudaEventRecord(prof_events[ev], s));
+  return ev;
+}
+
+void Engine::prof_end(cudaStream_t s, int ev, int cls, double flops, double bytes) {
+  if (ev < 0) return;
+  CK(cudaEventRecord(prof_events[ev + 1], s));
+  prof_recs.push_back(ProfRec{ev, cls, flops, bytes});
+}
+
+void Engine::prof_collect() {
+  for (const ProfRec& r : prof_recs) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, prof_events[r.ev], prof_events[r.ev + 1]));
+    prof_ms[r.cls] += ms;
+    prof_n[r.cls] += 1;
+    prof_flops[r.cls] += r.flops;
+    prof_bytes[r.cls] += r.bytes;
+  }
+  prof_recs.clear();
+  prof_used = 0;
+}
+
 Engine::~Engine() {
+  for (cudaEvent_t e : prof_events) cudaEventDestroy(e);
   cudaSetDevice(device);
   if (graph_exec) cudaGraphExecDestroy(graph_exec);
   if (stream) cudaStreamSynchronize(stream);
@@ -378,7 +424,7 @@ void Engine::reserve(int tok_cap, int row_cap, int64_t pool_cap) {
     return p;
   };
   const int d = arch.d_model, es = dtype_size(dt);
-  const int fe = arch.ffn_dim_enc, fd = std::max(arch.ffn_dim_dec, 1);
+  const int fe = arch.ffn_dim_enc, fd = std::max(arch.ffn_dim_dec, 8);
   ws.tok_cap = tok_cap;
   ws.row_cap = row_cap;
   ws.pool_cap = pool_cap;
@@ -461,7 +507,11 @@ void Engine::gemm(const void* A, const CUtensorMap* tmA, int lda, const Lin& L, 
   g.relu = relu;
   g.tmap_a = tmA;
   g.tmap_w = dt == kF32 ? nullptr : &L.tm;
+  const int ev = prof_begin(s);
   CK(launch_gemm(g, s));
+  prof_end(s, ev, gemm_cls, 2.0 * M * L.N * L.K,
+           (double)M * L.K * dtype_size(dt) + (double)L.N * L.K * dtype_size(dt) +
+               (double)M * L.N * dtype_size(c_dtype));
   ++launches;
 }
 
@@ -481,14 +531,20 @@ void Engine::gemm_argmax(const void* A, const CUtensorMap* tmA, int lda, int M,
   g.keys = keys;
   g.tmap_a = tmA;
   g.tmap_w = dt == kF32 ? nullptr : &out.tm;
+  const int ev = prof_begin(s);
   CK(launch_gemm(g, s));
+  prof_end(s, ev, FNMT_K_VOCAB, 2.0 * M * out.N * out.K,
+           (double)M * out.K * dtype_size(dt) + (double)out.N * out.K * dtype_size(dt));
   ++launches;
 }
 
 void Engine::norm(const float* x, const float* y, const Norm& n, float* o32, void* oa, int rows,
                   cudaStream_t s) {
+  const int ev = prof_begin(s);
   CK(launch_add_norm(x, y, n.g, n.b, arch.norm_l1, o32, dt == kF32 ? nullptr : oa,
                      dt, rows, arch.d_model, s));
+  prof_end(s, ev, FNMT_K_NORM, 0.0,
+           (double)rows * arch.d_model * (12.0 + (dt == kF32 ? 0 : dtype_size(dt))));
   ++launches;
 }
 
@@ -498,6 +554,7 @@ void Engine::encoder_layers(int n_tok, int n_seq, int max_q, int max_k, const in
                             int k_pad, cudaStream_t s) {
   const int d = arch.d_model;
   const bool tc = dt != kF32;
+  gemm_cls = FNMT_K_GEMM_ENC;
   for (const EncL& L : enc) {
     gemm(ws.xa, tc ? &ws.tm_xa : nullptr, d, L.qkv, n_tok, ws.qkv, 3 * d, dt, 0, s);
     AttnArgs a{};
@@ -519,7 +576,11 @@ void Engine::encoder_layers(int n_tok, int n_seq, int max_q, int max_k, const in
     a.n_seq = n_seq;
     a.max_q = max_q;
     a.max_k = std::max(max_k, k_pad);
-    CK(launch_attention_varlen(a, s));
+    {
+      const int ev = prof_begin(s);
+      CK(launch_attention_varlen(a, s));
+      prof_end(s, ev, FNMT_K_ATTN_ENC, 0.0, (double)n_tok * 4 * d * dtype_size(dt));
+    }
     ++launches;
     gemm(ws.att, tc ? &ws.tm_att : nullptr, d, L.o, n_tok, ws.y32, d, kF32, 0, s);
     norm(ws.x32, ws.y32, L.n1, ws.x32, ws.xa, n_tok, s);
@@ -531,6 +592,7 @@ void Engine::encoder_layers(int n_tok, int n_seq, int max_q, int max_k, const in
 
 void Engine::cross_kv_all(int n_tok, cudaStream_t s) {
   const int d = arch.d_model;
+  gemm_cls = FNMT_K_GEMM_ENC;
   for (int l = 0; l < arch.n_dec_layers; ++l)
     gemm(ws.xa, dt != kF32 ? &ws.tm_xa : nullptr, d, dec[l].ckv, n_tok, ws.ckv[l], 2 * d, dt, 0, s);
 }
@@ -542,8 +604,13 @@ void Engine::run_step(const StepView& v, cudaStream_t s) {
   const int d = arch.d_model, es = dtype_size(dt);
   const bool tc = dt != kF32;
   const int R = v.rows;
-  CK(launch_embed(v.prev, nullptr, v.t_ptr, tgt_emb32, pos32, emb_scale(), ws.dx32,
-                  tc ? ws.dxa : nullptr, dt, R, d, s));
+  gemm_cls = FNMT_K_GEMM_DEC;
+  {
+    const int ev = prof_begin(s);
+    CK(launch_embed(v.prev, nullptr, v.t_ptr, tgt_emb32, pos32, emb_scale(), ws.dx32,
+                    tc ? ws.dxa : nullptr, dt, R, d, s));
+    prof_end(s, ev, FNMT_K_EMBED, 0.0, (double)R * d * (8.0 + dtype_size(dt)));
+  }
   ++launches;
   for (int l = 0; l < arch.n_dec_layers; ++l) {
     const DecL& L = dec[l];
@@ -570,7 +637,11 @@ void Engine::run_step(const StepView& v, cudaStream_t s) {
     a.t_ptr = v.t_ptr;
     a.anc = v.anc;
     a.max_k = v.cap;
-    CK(launch_attention_decode(a, s));
+    {
+      const int ev = prof_begin(s);
+      CK(launch_attention_decode(a, s));
+      prof_end(s, ev, FNMT_K_ATTN_DEC, 0.0, (double)R * (v.host_t + 1) * 2 * d * es);
+    }
     ++launches;
     gemm(ws.datt, tc ? &ws.tm_datt : nullptr, d, L.so, R, ws.dy32, d, kF32, 0, s);
     norm(ws.dx32, ws.dy32, L.n1, ws.dx32, ws.dxa, R, s);
@@ -593,7 +664,11 @@ void Engine::run_step(const StepView& v, cudaStream_t s) {
     c.k_pad = v.k_pad;
     c.rows_per_seq = v.rows_per_seq;
     c.max_k = v.max_k;
-    CK(launch_attention_decode(c, s));
+    {
+      const int ev = prof_begin(s);
+      CK(launch_attention_decode(c, s));
+      prof_end(s, ev, FNMT_K_ATTN_DEC, 0.0, (double)R * v.max_k * 2 * d * es);
+    }
     ++launches;
     gemm(ws.datt, tc ? &ws.tm_datt : nullptr, d, L.co, R, ws.dy32, d, kF32, 0, s);
     norm(ws.dx32, ws.dy32, L.n2, ws.dx32, ws.dxa, R, s);
@@ -704,8 +779,10 @@ void Engine::translate_device(const int32_t* d_ids, const int64_t* d_off,
       cap = std::max(cap, budget_all[batch_row0[bi] + r]);
     }
     // 1) gather this batch's source ids into the packed workspace
+    int ev = prof_begin(stream);
     gather_batch_kernel<<<R, 128, 0, stream>>>(d_ids, d_off, perm_b, cu_b, R, ws.ids, ws.pos);
     CK(cudaGetLastError());
+    prof_end(stream, ev, FNMT_K_OTHER, 0.0, (double)n_tok * 12);
     ++launches;
     // per-sequence tables: q/k start = cu, len = cu diff
     CK(cudaMemcpyAsync(ws.cu, cu_b, sizeof(int32_t) * (R + 1), cudaMemcpyDeviceToDevice, stream));
@@ -713,8 +790,10 @@ void Engine::translate_device(const int32_t* d_ids, const int64_t* d_off,
                        cudaMemcpyDeviceToDevice, stream));
     lens_from_cu(R);
     // 2) encoder (packed varlen: only real tokens are rows)
+    ev = prof_begin(stream);
     CK(launch_embed(ws.ids, ws.pos, nullptr, src_emb32, pos32, emb_scale(), ws.x32,
                     dt != kF32 ? ws.xa : nullptr, dt, n_tok, arch.d_model, stream));
+    prof_end(stream, ev, FNMT_K_EMBED, 0.0, (double)n_tok * arch.d_model * (12.0 + dtype_size(dt)));
     ++launches;
     encoder_layers(n_tok, R, b.max_len, b.max_len, ws.cu, ws.len, ws.cu, ws.len, 0, stream);
     cross_kv_all(n_tok, stream);
@@ -750,16 +829,28 @@ void Engine::translate_device(const int32_t* d_ids, const int64_t* d_off,
     gs.out_cap = cap;
     gs.eos = run.eos_id;
     gs.pad = run.pad_id;
-    const int64_t nodes = capture_step(v, gs);
+    const int64_t nodes = profiling ? 0 : capture_step(v, gs);
     const int chunk = 8;
     int steps = 0;
     int inflight = 0;
     bool stop = false;
     for (int c0 = 0; c0 < cap && !stop; c0 += chunk) {
       const int c1 = std::min(cap, c0 + chunk);
-      for (int t = c0; t < c1; ++t) CK(cudaGraphLaunch(graph_exec, stream));
+      if (profiling) {
+        // un-captured launches so every kernel can be bracketed by events
+        for (int t = c0; t < c1; ++t) {
+          v.host_t = t;
+          run_step(v, stream);
+          const int ev = prof_begin(stream);
+          CK(launch_greedy_update(gs, stream));
+          prof_end(stream, ev, FNMT_K_SEARCH, 0.0, (double)R * 24);
+          ++launches;
+        }
+      } else {
+        for (int t = c0; t < c1; ++t) CK(cudaGraphLaunch(graph_exec, stream));
+        launches += nodes * (c1 - c0);
+      }
       steps += c1 - c0;
-      launches += nodes * (c1 - c0);
       const int slot = (c0 / chunk) & 1;
       if (inflight == 2) {
         // wait for the chunk before the previous one; stop when every row finished
@@ -773,14 +864,17 @@ void Engine::translate_device(const int32_t* d_ids, const int64_t* d_off,
     }
     steps_total += steps;
     // 4) restore order: scatter rows to their sentence slots
+    ev = prof_begin(stream);
     scatter_out_kernel<<<R, 64, 0, stream>>>(ws.out_ids, ws.out_len, cap, perm_b, R, d_out_off,
                                             d_out_ids, d_out_len);
     CK(cudaGetLastError());
+    prof_end(stream, ev, FNMT_K_OTHER, 0.0, (double)R * cap * 8);
     ++launches;
     tgt_capacity += n_tok;
   }
   CK(cudaEventRecord(ev_t1, stream));
   CK(cudaStreamSynchronize(stream));
+  if (profiling) prof_collect();
   if (st) {
     float ms = 0.f;
     cudaEventElapsedTime(&ms, ev_t0, ev_t1);

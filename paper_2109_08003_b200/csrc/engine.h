@@ -80,6 +80,7 @@ struct StepView {
   const int32_t* k_len = nullptr;
   int k_pad = 0, rows_per_seq = 1, max_k = 0;
   const int32_t* anc = nullptr;
+  int host_t = 0;                      // host copy of the step (profiling byte counts only)
   unsigned long long* keys = nullptr;  // argmax output (greedy)
   float* logits = nullptr;             // or full logits (protocol path)
 };
@@ -113,7 +114,28 @@ class Engine {
   int64_t device_bytes = 0;
   int64_t launches = 0;
 
+  // Per-kernel-class profiling (CUDA events around every launch; disables
+  // graph capture while on).  Totals are folded in after each translate call.
+  void set_profiling(bool on);
+  bool profiling = false;
+  double prof_ms[FNMT_K_COUNT] = {};
+  int64_t prof_n[FNMT_K_COUNT] = {};
+  double prof_flops[FNMT_K_COUNT] = {};
+  double prof_bytes[FNMT_K_COUNT] = {};
+
  private:
+  int prof_begin(cudaStream_t s);
+  void prof_end(cudaStream_t s, int ev, int cls, double flops, double bytes);
+  void prof_collect();
+  struct ProfRec {
+    int ev, cls;
+    double flops, bytes;
+  };
+  std::vector<cudaEvent_t> prof_events;
+  std::vector<ProfRec> prof_recs;
+  size_t prof_used = 0;
+  int gemm_cls = FNMT_K_GEMM_ENC;
+
   void* dalloc(size_t bytes);
   const std::vector<float>& need(const std::string& name, int64_t numel) const;
   float* upload_f32(const std::vector<float>& v);

@@ -118,6 +118,18 @@ class Engine:
     def device_bytes(self) -> int:
         return self.handle.device_bytes()
 
+    def profile(self, on: bool = True):
+        """Bracket every engine launch with CUDA events (decode runs un-captured)."""
+        check(lib.fnmt_engine_profile(self.handle.h, int(on)), "profile")
+
+    def profile_read(self) -> dict:
+        n = len(_capi.KERNEL_CLASSES)
+        ms, cnt = (C.c_double * n)(), (C.c_int64 * n)()
+        fl, by = (C.c_double * n)(), (C.c_double * n)()
+        check(lib.fnmt_engine_profile_read(self.handle.h, ms, cnt, fl, by), "profile_read")
+        return {name: {"ms": ms[i], "launches": cnt[i], "flops": fl[i], "bytes": by[i]}
+                for i, name in enumerate(_capi.KERNEL_CLASSES)}
+
 
 def translate_ids(handle, rows, search=None, sbatch=3072, wbatch=64000) -> list[list[int]]:
     """Greedy-translate a list of id sequences through the native corpus path."""

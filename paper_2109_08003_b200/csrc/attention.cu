@@ -2,7 +2,7 @@
 //
 // Semantics kept from the reference:
 //  * the query is scaled by f32(1/sqrt(dk)) before the score product
-//    (model.py:223, "exact reorder" of score scaling);
+//    (model.py:223, the "exact reorder" of score scaling);
 //  * softmax subtracts the row max, exponentiates, divides by the row sum
 //    (tensor.py:70-81); weights are normalised before the value product;
 //  * masked keys carry an additive -1e9 (model.py:37-38, :243-245).  For a
@@ -11,14 +11,20 @@
 //    ALL masked attends over every padded key with the -1e9 offset applied,
 //    exactly like the reference.
 //
-// Two kernels:
-//  * attention_varlen_kernel — encoder self-attention over packed varlen
-//    sequences.  CTA = (16-query tile, sequence, head).  Q tile, a 32-key K/V
-//    tile, the score rows and the output accumulator are staged in shared
-//    memory (padded rows, conflict-free); fp32 math throughout.
-//  * attention_decode_kernel — one query per row against the self-KV cache
+// Kernels (fp32 math everywhere, storage T = f32 / f16 / bf16):
+//  * attn_varlen_kernel — encoder self-attention over packed varlen
+//    sequences.  CTA = (32-query tile, sequence, head), 256 threads.  Both
+//    contractions are register-tiled mini-GEMMs through shared memory:
+//    scores = Q K^T in (32 q x 64 k) tiles over 32-dim chunks (2x4 outputs
+//    per thread), the full score rows stay in shared memory for the
+//    softmax, then O = P V in (32 q x 64 d) tiles over 32-key chunks.
+//  * attn_decode_kernel — one query per row against the self-KV cache
 //    (appending this step's k/v first) or the cached cross K/V.  CTA =
-//    (row, head); warps stride over keys, lanes over head dims.
+//    (row, head), 128 threads; G lanes per key with 16-byte vector loads,
+//    32/G keys per warp in flight; value product split over key groups and
+//    reduced in a fixed order (deterministic).
+//  * attn_decode_generic — scalar fallback for head sizes that are not a
+//    multiple of one 16-byte vector (tiny test models).
 #include <math.h>
 
 #include "common.cuh"
@@ -28,22 +34,56 @@ namespace fnmt {
 
 namespace {
 
-constexpr int kQT = 16;   // queries per CTA
-constexpr int kKT = 32;   // keys per smem tile
-constexpr int kThreads = 128;
 constexpr float kMaskValue = -1e9f;
 
 template <typename T>
-__global__ void __launch_bounds__(kThreads)
-    attention_varlen_kernel(AttnArgs a, float qscale, int kcap) {
-  extern __shared__ float sm[];
-  const int dk = a.dk;
-  const int ldp = dk + 1;
-  float* Qs = sm;                    // [kQT][dk+1]
-  float* KV = Qs + kQT * ldp;        // [kKT][dk+1]
-  float* O = KV + kKT * ldp;         // [kQT][dk]
-  float* P = O + kQT * dk;           // [kQT][kcap]
+struct Vec16 {
+  static constexpr int N = 16 / sizeof(T);
+};
 
+__device__ __forceinline__ void load16(const float* p, float (&f)[4]) {
+  const float4 v = *reinterpret_cast<const float4*>(p);
+  f[0] = v.x; f[1] = v.y; f[2] = v.z; f[3] = v.w;
+}
+__device__ __forceinline__ void load16(const __half* p, float (&f)[8]) {
+  const uint4 u = *reinterpret_cast<const uint4*>(p);
+  const __half2* h = reinterpret_cast<const __half2*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 x = __half22float2(h[i]);
+    f[2 * i] = x.x;
+    f[2 * i + 1] = x.y;
+  }
+}
+__device__ __forceinline__ void load16(const __nv_bfloat16* p, float (&f)[8]) {
+  const uint4 u = *reinterpret_cast<const uint4*>(p);
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 x = __bfloat1622float2(h[i]);
+    f[2 * i] = x.x;
+    f[2 * i + 1] = x.y;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// encoder varlen attention
+
+constexpr int kQT = 32;   // queries per CTA
+constexpr int kKT = 64;   // keys per score tile
+constexpr int kDC = 32;   // head dims per score-chunk
+constexpr int kPK = 32;   // keys per value-chunk
+constexpr int kPD = 64;   // head dims per output tile
+constexpr int kVThreads = 256;
+
+template <typename T>
+__global__ void __launch_bounds__(kVThreads)
+    attn_varlen_kernel(AttnArgs a, float qscale, int kcap) {
+  extern __shared__ float sm[];
+  float* S = sm;                               // [kQT][kcap]
+  float* Qs = S + kQT * kcap;                  // [kDC][kQT + 4]   dim-major
+  float* Ks = Qs + kDC * (kQT + 4);            // [kDC][kKT + 4]   dim-major  (also V tile)
+  const int dk = a.dk;
   const int b = blockIdx.y, h = blockIdx.z;
   const int q0 = blockIdx.x * kQT;
   const int nq = a.q_len[b];
@@ -51,48 +91,62 @@ __global__ void __launch_bounds__(kThreads)
   const int kl = a.k_len[b];
   const bool all_masked = kl == 0;
   const int nk = all_masked ? a.k_pad : kl;
-  const int qrow0 = a.q_start[b] + q0;
-  const int krow0 = a.k_start[b];
   const int qn = min(kQT, nq - q0);
-  const T* q = reinterpret_cast<const T*>(a.q);
-  const T* k = reinterpret_cast<const T*>(a.k);
-  const T* v = reinterpret_cast<const T*>(a.v);
+  const int64_t qrow0 = a.q_start[b] + q0;
+  const int64_t krow0 = a.k_start[b];
+  const T* q = reinterpret_cast<const T*>(a.q) + h * dk;
+  const T* k = reinterpret_cast<const T*>(a.k) + h * dk;
+  const T* v = reinterpret_cast<const T*>(a.v) + h * dk;
   const int tid = threadIdx.x;
-  const int warp = tid >> 5, lane = tid & 31;
+  const int tq = tid >> 4;   // 0..15 -> query rows 2*tq, 2*tq+1
+  const int tc = tid & 15;   // 0..15 -> columns 4*tc .. 4*tc+3
 
-  for (int i = tid; i < kQT * dk; i += kThreads) {
-    const int qi = i / dk, e = i - qi * dk;
-    float val = 0.f;
-    if (qi < qn) val = to_f32(q[(size_t)(qrow0 + qi) * a.ldq + h * dk + e]) * qscale;
-    Qs[qi * ldp + e] = val;
-    O[i] = 0.f;
-  }
-
-  // pass 1: scores
-  for (int kt = 0; kt < nk; kt += kKT) {
-    const int kn = min(kKT, nk - kt);
-    __syncthreads();
-    for (int i = tid; i < kKT * dk; i += kThreads) {
-      const int j = i / dk, e = i - j * dk;
-      KV[j * ldp + e] = j < kn ? to_f32(k[(size_t)(krow0 + kt + j) * a.ldkv + h * dk + e]) : 0.f;
-    }
-    __syncthreads();
-    for (int p = tid; p < kQT * kKT; p += kThreads) {
-      const int qi = p / kKT, j = p - qi * kKT;
-      if (qi < qn && j < kn) {
-        const float* qr = Qs + qi * ldp;
-        const float* kr = KV + j * ldp;
-        float s = 0.f;
-        for (int e = 0; e < dk; ++e) s = fmaf(qr[e], kr[e], s);
-        if (all_masked) s = s + kMaskValue;
-        P[qi * kcap + kt + j] = s;
+  // ---- scores S = (q * scale) K^T --------------------------------------------
+  for (int k0 = 0; k0 < nk; k0 += kKT) {
+    float acc[2][4] = {};
+    for (int d0 = 0; d0 < dk; d0 += kDC) {
+      __syncthreads();
+      for (int i = tid; i < kQT * kDC; i += kVThreads) {
+        const int qi = i / kDC, dd = i % kDC;
+        float val = 0.f;
+        if (qi < qn && d0 + dd < dk) val = to_f32(q[(qrow0 + qi) * a.ldq + d0 + dd]) * qscale;
+        Qs[dd * (kQT + 4) + qi] = val;
+      }
+      for (int i = tid; i < kKT * kDC; i += kVThreads) {
+        const int kj = i / kDC, dd = i % kDC;
+        float val = 0.f;
+        if (k0 + kj < nk && d0 + dd < dk) val = to_f32(k[(krow0 + k0 + kj) * a.ldkv + d0 + dd]);
+        Ks[dd * (kKT + 4) + kj] = val;
+      }
+      __syncthreads();
+#pragma unroll 8
+      for (int dd = 0; dd < kDC; ++dd) {
+        const float2 qv = *reinterpret_cast<const float2*>(Qs + dd * (kQT + 4) + 2 * tq);
+        const float4 kv = *reinterpret_cast<const float4*>(Ks + dd * (kKT + 4) + 4 * tc);
+        acc[0][0] = fmaf(qv.x, kv.x, acc[0][0]);
+        acc[0][1] = fmaf(qv.x, kv.y, acc[0][1]);
+        acc[0][2] = fmaf(qv.x, kv.z, acc[0][2]);
+        acc[0][3] = fmaf(qv.x, kv.w, acc[0][3]);
+        acc[1][0] = fmaf(qv.y, kv.x, acc[1][0]);
+        acc[1][1] = fmaf(qv.y, kv.y, acc[1][1]);
+        acc[1][2] = fmaf(qv.y, kv.z, acc[1][2]);
+        acc[1][3] = fmaf(qv.y, kv.w, acc[1][3]);
       }
     }
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int qi = 2 * tq + i, kj = k0 + 4 * tc + j;
+        if (qi < qn && kj < nk) S[qi * kcap + kj] = all_masked ? acc[i][j] + kMaskValue : acc[i][j];
+      }
   }
   __syncthreads();
-  // softmax per query row (warp per row)
-  for (int qi = warp; qi < qn; qi += kThreads / 32) {
-    float* pr = P + qi * kcap;
+
+  // ---- softmax per query row (warp per row) ----------------------------------
+  const int warp = tid >> 5, lane = tid & 31;
+  for (int qi = warp; qi < qn; qi += kVThreads / 32) {
+    float* pr = S + qi * kcap;
     float mx = -INFINITY;
     for (int j = lane; j < nk; j += 32) mx = fmaxf(mx, pr[j]);
     mx = warp_max(mx);
@@ -105,136 +159,270 @@ __global__ void __launch_bounds__(kThreads)
     sum = warp_sum(sum);
     for (int j = lane; j < nk; j += 32) pr[j] = pr[j] / sum;
   }
-  // pass 2: weights . V
-  for (int kt = 0; kt < nk; kt += kKT) {
-    const int kn = min(kKT, nk - kt);
-    __syncthreads();
-    for (int i = tid; i < kKT * dk; i += kThreads) {
-      const int j = i / dk, e = i - j * dk;
-      KV[j * ldp + e] = j < kn ? to_f32(v[(size_t)(krow0 + kt + j) * a.ldkv + h * dk + e]) : 0.f;
+
+  // ---- O = P V ------------------------------------------------------------------
+  float* Vs = Ks;   // [kPK][kPD + 4]  key-major
+  T* out = reinterpret_cast<T*>(a.out) + h * dk;
+  for (int d0 = 0; d0 < dk; d0 += kPD) {
+    float acc[2][4] = {};
+    for (int j0 = 0; j0 < nk; j0 += kPK) {
+      const int jn = min(kPK, nk - j0);
+      __syncthreads();
+      for (int i = tid; i < kPK * kPD; i += kVThreads) {
+        const int kj = i / kPD, dd = i % kPD;
+        float val = 0.f;
+        if (kj < jn && d0 + dd < dk) val = to_f32(v[(krow0 + j0 + kj) * a.ldkv + d0 + dd]);
+        Vs[kj * (kPD + 4) + dd] = val;
+      }
+      __syncthreads();
+      const float* p0 = S + (2 * tq) * kcap + j0;
+      const float* p1 = p0 + kcap;
+      for (int kj = 0; kj < jn; ++kj) {
+        const float w0 = p0[kj], w1 = p1[kj];
+        const float4 vv = *reinterpret_cast<const float4*>(Vs + kj * (kPD + 4) + 4 * tc);
+        acc[0][0] = fmaf(w0, vv.x, acc[0][0]);
+        acc[0][1] = fmaf(w0, vv.y, acc[0][1]);
+        acc[0][2] = fmaf(w0, vv.z, acc[0][2]);
+        acc[0][3] = fmaf(w0, vv.w, acc[0][3]);
+        acc[1][0] = fmaf(w1, vv.x, acc[1][0]);
+        acc[1][1] = fmaf(w1, vv.y, acc[1][1]);
+        acc[1][2] = fmaf(w1, vv.z, acc[1][2]);
+        acc[1][3] = fmaf(w1, vv.w, acc[1][3]);
+      }
     }
-    __syncthreads();
-    for (int i = tid; i < qn * dk; i += kThreads) {
-      const int qi = i / dk, e = i - qi * dk;
-      const float* pr = P + qi * kcap + kt;
-      float acc = O[i];
-      for (int j = 0; j < kn; ++j) acc = fmaf(pr[j], KV[j * ldp + e], acc);
-      O[i] = acc;
-    }
-  }
-  __syncthreads();
-  T* out = reinterpret_cast<T*>(a.out);
-  for (int i = tid; i < qn * dk; i += kThreads) {
-    const int qi = i / dk, e = i - qi * dk;
-    out[(size_t)(qrow0 + qi) * a.ldo + h * dk + e] = from_f32<T>(O[i]);
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int qi = 2 * tq + i, dd = d0 + 4 * tc + j;
+        if (qi < qn && dd < dk) out[(qrow0 + qi) * a.ldo + dd] = from_f32<T>(acc[i][j]);
+      }
   }
 }
 
-template <typename T>
-__global__ void __launch_bounds__(kThreads)
-    attention_decode_kernel(DecAttnArgs a, float qscale) {
-  extern __shared__ float sm[];
-  const int dk = a.dk;
-  float* qs = sm;          // [dk]
-  float* S = sm + dk;      // [max_k]
-  const int r = blockIdx.x, h = blockIdx.y;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const T* kbase = reinterpret_cast<const T*>(a.k);
-  const T* vbase = reinterpret_cast<const T*>(a.v);
+// ---------------------------------------------------------------------------
+// decode attention (one query per row)
 
+constexpr int kDThreads = 128;
+
+struct DecCtx {
   int nk;
-  bool all_masked = false;
-  int t = 0;
-  int64_t seq_row0 = 0;
+  bool all_masked;
+  int t;
+  int64_t seq_row0;
+};
+
+template <typename T>
+__device__ __forceinline__ DecCtx decode_setup(const DecAttnArgs& a, int r, int h) {
+  DecCtx c{};
   if (a.self_mode) {
-    t = *a.t_ptr;
-    nk = t + 1;
-    // append this step's key/value (this head's slice) at slot t
+    c.t = *a.t_ptr;
+    c.nk = c.t + 1;
     T* kw = reinterpret_cast<T*>(a.k_w);
     T* vw = reinterpret_cast<T*>(a.v_w);
-    const T* nkp = reinterpret_cast<const T*>(a.new_k) + (size_t)r * a.ld_new + h * dk;
-    const T* nvp = reinterpret_cast<const T*>(a.new_v) + (size_t)r * a.ld_new + h * dk;
-    const size_t slot = ((size_t)r * a.cap + t) * a.ldkv + h * dk;
-    for (int e = tid; e < dk; e += kThreads) {
+    const T* nkp = reinterpret_cast<const T*>(a.new_k) + (size_t)r * a.ld_new + h * a.dk;
+    const T* nvp = reinterpret_cast<const T*>(a.new_v) + (size_t)r * a.ld_new + h * a.dk;
+    const size_t slot = ((size_t)r * a.cap + c.t) * a.ldkv + h * a.dk;
+    for (int e = threadIdx.x; e < a.dk; e += blockDim.x) {
       kw[slot + e] = nkp[e];
       vw[slot + e] = nvp[e];
     }
   } else {
     const int seq = r / a.rows_per_seq;
     const int kl = a.k_len[seq];
-    all_masked = kl == 0;
-    nk = all_masked ? a.k_pad : kl;
-    seq_row0 = a.k_start[seq];
+    c.all_masked = kl == 0;
+    c.nk = c.all_masked ? a.k_pad : kl;
+    c.seq_row0 = a.k_start[seq];
   }
+  return c;
+}
+
+__device__ __forceinline__ int64_t decode_key_row(const DecAttnArgs& a, const DecCtx& c, int r,
+                                                  int j) {
+  if (a.self_mode) {
+    const int src = (a.anc && j < c.t) ? a.anc[(size_t)r * a.cap + j] : r;
+    return (int64_t)src * a.cap + j;
+  }
+  return c.seq_row0 + j;
+}
+
+__device__ __forceinline__ void softmax_inplace(float* S, int nk) {
+  const int lane = threadIdx.x & 31;
+  float mx = -INFINITY;
+  for (int j = lane; j < nk; j += 32) mx = fmaxf(mx, S[j]);
+  mx = warp_max(mx);
+  float sum = 0.f;
+  for (int j = lane; j < nk; j += 32) {
+    const float e = expf(S[j] - mx);
+    S[j] = e;
+    sum += e;
+  }
+  sum = warp_sum(sum);
+  for (int j = lane; j < nk; j += 32) S[j] = S[j] / sum;
+}
+
+// G lanes cooperate on one key (CH 16-byte chunks each); 32/G keys per warp.
+template <typename T, int G, int CH>
+__global__ void __launch_bounds__(kDThreads) attn_decode_kernel(DecAttnArgs a, float qscale) {
+  constexpr int VEC = Vec16<T>::N;
+  extern __shared__ float sm[];
+  const int dk = a.dk;
+  float* qs = sm;                  // [dk]
+  float* S = qs + dk;              // [max_k]
+  float* red = S + a.max_k + 4;    // [groups][dk]
+  const int r = blockIdx.x, h = blockIdx.y;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const DecCtx c = decode_setup<T>(a, r, h);
   const T* q = reinterpret_cast<const T*>(a.q) + (size_t)r * a.ldq + h * dk;
-  for (int e = tid; e < dk; e += kThreads) qs[e] = to_f32(q[e]) * qscale;
+  for (int e = tid; e < dk; e += kDThreads) qs[e] = to_f32(q[e]) * qscale;
   __syncthreads();
 
-  auto key_row = [&](int j) -> int64_t {
-    if (a.self_mode) {
-      const int src = (a.anc && j < t) ? a.anc[(size_t)r * a.cap + j] : r;
-      return (int64_t)src * a.cap + j;
-    }
-    return seq_row0 + j;
-  };
-
-  for (int j = warp; j < nk; j += kThreads / 32) {
-    const T* kr = kbase + key_row(j) * a.ldkv + h * dk;
+  const T* kb = reinterpret_cast<const T*>(a.k) + h * dk;
+  constexpr int KPW = 32 / G;
+  const int g = lane / G, li = lane % G;
+  for (int j0 = warp * KPW; j0 < c.nk; j0 += (kDThreads / 32) * KPW) {
+    const int j = j0 + g;
     float s = 0.f;
-    for (int e = lane; e < dk; e += 32) s = fmaf(qs[e], to_f32(kr[e]), s);
-    s = warp_sum(s);
-    if (lane == 0) S[j] = all_masked ? s + kMaskValue : s;
+    if (j < c.nk) {
+      const T* kr = kb + decode_key_row(a, c, r, j) * a.ldkv;
+#pragma unroll
+      for (int ch = 0; ch < CH; ++ch) {
+        const int e0 = (li + ch * G) * VEC;
+        if (e0 < dk) {
+          float f[VEC];
+          load16(kr + e0, f);
+#pragma unroll
+          for (int i = 0; i < VEC; ++i) s = fmaf(qs[e0 + i], f[i], s);
+        }
+      }
+    }
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (li == 0 && j < c.nk) S[j] = c.all_masked ? s + kMaskValue : s;
   }
   __syncthreads();
-  if (warp == 0) {
-    float mx = -INFINITY;
-    for (int j = lane; j < nk; j += 32) mx = fmaxf(mx, S[j]);
-    mx = warp_max(mx);
-    float sum = 0.f;
-    for (int j = lane; j < nk; j += 32) {
-      const float e = expf(S[j] - mx);
-      S[j] = e;
-      sum += e;
+  if (warp == 0) softmax_inplace(S, c.nk);
+  __syncthreads();
+
+  // value product: thread = (chunk, key group)
+  const int nch = dk / VEC;
+  const int groups = kDThreads / nch;
+  const int ch = tid % nch, grp = tid / nch;
+  const T* vb = reinterpret_cast<const T*>(a.v) + h * dk + ch * VEC;
+  float acc[VEC];
+#pragma unroll
+  for (int i = 0; i < VEC; ++i) acc[i] = 0.f;
+  if (grp < groups) {
+    for (int j = grp; j < c.nk; j += groups) {
+      float f[VEC];
+      load16(vb + decode_key_row(a, c, r, j) * a.ldkv, f);
+      const float w = S[j];
+#pragma unroll
+      for (int i = 0; i < VEC; ++i) acc[i] = fmaf(w, f[i], acc[i]);
     }
-    sum = warp_sum(sum);
-    for (int j = lane; j < nk; j += 32) S[j] = S[j] / sum;
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) red[grp * dk + ch * VEC + i] = acc[i];
   }
   __syncthreads();
   T* out = reinterpret_cast<T*>(a.out) + (size_t)r * a.ldo + h * dk;
-  for (int e = tid; e < dk; e += kThreads) {
-    float acc = 0.f;
-    for (int j = 0; j < nk; ++j) acc = fmaf(S[j], to_f32(vbase[key_row(j) * a.ldkv + h * dk + e]), acc);
-    out[e] = from_f32<T>(acc);
+  for (int e = tid; e < dk; e += kDThreads) {
+    float sum = red[e];
+    for (int gg = 1; gg < groups; ++gg) sum += red[gg * dk + e];
+    out[e] = from_f32<T>(sum);
   }
 }
 
 template <typename T>
+__global__ void __launch_bounds__(kDThreads) attn_decode_generic(DecAttnArgs a, float qscale) {
+  extern __shared__ float sm[];
+  const int dk = a.dk;
+  float* qs = sm;
+  float* S = sm + dk;
+  const int r = blockIdx.x, h = blockIdx.y;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const DecCtx c = decode_setup<T>(a, r, h);
+  const T* q = reinterpret_cast<const T*>(a.q) + (size_t)r * a.ldq + h * dk;
+  for (int e = tid; e < dk; e += kDThreads) qs[e] = to_f32(q[e]) * qscale;
+  __syncthreads();
+  const T* kb = reinterpret_cast<const T*>(a.k) + h * dk;
+  const T* vb = reinterpret_cast<const T*>(a.v) + h * dk;
+  for (int j = warp; j < c.nk; j += kDThreads / 32) {
+    const T* kr = kb + decode_key_row(a, c, r, j) * a.ldkv;
+    float s = 0.f;
+    for (int e = lane; e < dk; e += 32) s = fmaf(qs[e], to_f32(kr[e]), s);
+    s = warp_sum(s);
+    if (lane == 0) S[j] = c.all_masked ? s + kMaskValue : s;
+  }
+  __syncthreads();
+  if (warp == 0) softmax_inplace(S, c.nk);
+  __syncthreads();
+  T* out = reinterpret_cast<T*>(a.out) + (size_t)r * a.ldo + h * dk;
+  for (int e = tid; e < dk; e += kDThreads) {
+    float acc = 0.f;
+    for (int j = 0; j < c.nk; ++j) acc = fmaf(S[j], to_f32(vb[decode_key_row(a, c, r, j) * a.ldkv + e]), acc);
+    out[e] = from_f32<T>(acc);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// dispatch
+
+template <typename T>
 cudaError_t varlen_dispatch(const AttnArgs& a, cudaStream_t s) {
-  const int kcap = ((a.max_k + 31) / 32) * 32;
-  const size_t smem = sizeof(float) * ((size_t)kQT * (a.dk + 1) + (size_t)kKT * (a.dk + 1) +
-                                       (size_t)kQT * a.dk + (size_t)kQT * kcap);
+  const int kcap = ((a.max_k + kKT - 1) / kKT) * kKT;
+  const size_t smem =
+      sizeof(float) * ((size_t)kQT * kcap + (size_t)kDC * (kQT + 4) + (size_t)kDC * (kKT + 4));
+  static_assert(kDC * (kKT + 4) >= kPK * (kPD + 4), "V tile must fit in the K tile region");
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
-  cudaError_t e = cudaFuncSetAttribute(attention_varlen_kernel<T>,
+  cudaError_t e = cudaFuncSetAttribute(attn_varlen_kernel<T>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   dim3 grid((a.max_q + kQT - 1) / kQT, a.n_seq, a.heads);
   const float qscale = (float)(1.0 / sqrt((double)a.dk));
-  attention_varlen_kernel<T><<<grid, kThreads, smem, s>>>(a, qscale, kcap);
+  attn_varlen_kernel<T><<<grid, kVThreads, smem, s>>>(a, qscale, kcap);
+  return cudaGetLastError();
+}
+
+template <typename T, int G, int CH>
+cudaError_t launch_dec(const DecAttnArgs& a, float qscale, size_t smem, cudaStream_t s) {
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(attn_decode_kernel<T, G, CH>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  attn_decode_kernel<T, G, CH><<<dim3(a.rows, a.heads), kDThreads, smem, s>>>(a, qscale);
   return cudaGetLastError();
 }
 
 template <typename T>
 cudaError_t decode_dispatch(const DecAttnArgs& a, cudaStream_t s) {
+  constexpr int VEC = Vec16<T>::N;
+  const float qscale = (float)(1.0 / sqrt((double)a.dk));
+  const int nch = a.dk / VEC;
+  const bool vec_ok = a.dk % VEC == 0 && nch <= kDThreads && (a.ldkv % VEC) == 0;
+  if (vec_ok) {
+    const int groups = kDThreads / nch;
+    const size_t smem = sizeof(float) * ((size_t)a.dk + a.max_k + 4 + (size_t)groups * a.dk);
+    if (smem <= 227 * 1024) {
+      if (nch <= 1) return launch_dec<T, 1, 1>(a, qscale, smem, s);
+      if (nch <= 2) return launch_dec<T, 2, 1>(a, qscale, smem, s);
+      if (nch <= 4) return launch_dec<T, 4, 1>(a, qscale, smem, s);
+      if (nch <= 8) return launch_dec<T, 8, 1>(a, qscale, smem, s);
+      if (nch <= 16) return launch_dec<T, 16, 1>(a, qscale, smem, s);
+      if (nch <= 32) return launch_dec<T, 32, 1>(a, qscale, smem, s);
+      if (nch <= 64) return launch_dec<T, 32, 2>(a, qscale, smem, s);
+      if (nch <= 96) return launch_dec<T, 32, 3>(a, qscale, smem, s);
+      return launch_dec<T, 32, 4>(a, qscale, smem, s);
+    }
+  }
   const size_t smem = sizeof(float) * ((size_t)a.dk + (size_t)a.max_k + 32);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(attention_decode_kernel<T>,
+    cudaError_t e = cudaFuncSetAttribute(attn_decode_generic<T>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  dim3 grid(a.rows, a.heads);
-  const float qscale = (float)(1.0 / sqrt((double)a.dk));
-  attention_decode_kernel<T><<<grid, kThreads, smem, s>>>(a, qscale);
+  attn_decode_generic<T><<<dim3(a.rows, a.heads), kDThreads, smem, s>>>(a, qscale);
   return cudaGetLastError();
 }
 

@@ -5,17 +5,24 @@
 // epilogue, the vocab projection + `np.argmax` of greedy search
 // (model.py:344, search.py:71).
 //
-// * fp16 / bf16 path: hand-written tcgen05 kernel.  TMA (cp.async.bulk.tensor,
-//   128 B swizzle) streams 128x64 A tiles and BNx64 W tiles through a
-//   STAGES-deep mbarrier ring; one elected thread issues tcgen05.mma
-//   (kind::f16, M=128, N=BN, K=16) into a TMEM fp32 accumulator; four warps
-//   drain TMEM with tcgen05.ld and apply the fused epilogue.
+// * fp16 / bf16 path: persistent, warp-specialised tcgen05 kernel.
+//     warp 0      TMA producer: 128x64 A tiles and BNx64 W tiles
+//                 (cp.async.bulk.tensor, 128 B swizzle) into a STAGES-deep
+//                 mbarrier ring;
+//     warp 1      one elected thread issues tcgen05.mma (kind::f16, M=128,
+//                 N=BN, K=16) into one of two TMEM fp32 accumulators;
+//     warps 2..5  epilogue: tcgen05.ld the finished accumulator, apply
+//                 bias / residual / ReLU / dtype cast (or the argmax
+//                 reduction), release the TMEM buffer.
+//   The double-buffered accumulator lets the epilogue of tile i overlap the
+//   MMAs of tile i+1.  BN (64/128/256) is chosen per problem so that skinny
+//   decoder GEMMs still fill the 148 SMs.
 // * fp32 path (parity mode, TF32 off): SIMT kernel, fp32 FMA in ascending-k
 //   order.
 //
-// Both paths accumulate every output in a fixed k order that does not depend
-// on M, so a sentence's result never depends on its batch neighbours
-// (the reference's batch-invariance contract, tensor.py:8-12).
+// Every output is accumulated in a fixed k order that does not depend on M or
+// on the tile shape, so a sentence's result never depends on its batch
+// neighbours (the reference's batch-invariance contract, tensor.py:8-12).
 #include <cudaTypedefs.h>
 
 #include <mutex>
@@ -29,11 +36,8 @@ namespace {
 
 constexpr int kBM = 128;
 constexpr int kBK = 64;
-constexpr int kBN = 128;
-constexpr int kStages = 4;
+constexpr int kWBox = 64;   // W TMA box rows; BN/64 boxes per stage
 constexpr int kABytes = kBM * kBK * 2;
-constexpr int kBBytes = kBN * kBK * 2;
-constexpr int kTcSmem = 1024 + kStages * (kABytes + kBBytes) + 256;
 
 struct EpiParams {
   const float* bias;
@@ -66,133 +70,242 @@ __device__ __forceinline__ void store_elem(const EpiParams& e, int m, int n, flo
     reinterpret_cast<__nv_bfloat16*>(e.C)[off] = __float2bfloat16_rn(v);
 }
 
-// ---------------------------------------------------------------------------
-// tcgen05 kernel
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 
-__global__ void __launch_bounds__(128, 1)
+__device__ __forceinline__ void named_bar_sync(int id, int threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
+// Apply the epilogue to 32 consecutive accumulator columns of row m.  `bs`
+// holds the bias of these columns in shared memory (zeros past N).  For the
+// argmax epilogue the running (value, index) pair is kept in registers; a
+// strict '>' over ascending columns keeps the lowest index on ties.
+__device__ __forceinline__ void epilogue_chunk(const EpiParams& ep, int m, int nb,
+                                               const float (&v)[32], const float* bs,
+                                               float& best_v, int& best_i) {
+  if (ep.epi == kEpiArgmax) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const float x = v[i] + bs[i];
+      if (nb + i < ep.N && x > best_v) {
+        best_v = x;
+        best_i = nb + i;
+      }
+    }
+    return;
+  }
+  const bool full_chunk = nb + 32 <= ep.N;
+  if (full_chunk && ep.c_dtype != kF32 && (ep.ldc % 8) == 0 && ep.resid == nullptr) {
+    uint32_t packed[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      float a = v[2 * i] + bs[2 * i];
+      float b = v[2 * i + 1] + bs[2 * i + 1];
+      if (ep.relu) {
+        a = fmaxf(a, 0.f);
+        b = fmaxf(b, 0.f);
+      }
+      if (ep.c_dtype == kF16) {
+        __half2 h = __floats2half2_rn(a, b);
+        packed[i] = *reinterpret_cast<uint32_t*>(&h);
+      } else {
+        __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+        packed[i] = *reinterpret_cast<uint32_t*>(&h);
+      }
+    }
+    uint4* dst =
+        reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(ep.C) + (size_t)m * ep.ldc + nb);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      dst[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
+    return;
+  }
+  if (full_chunk && ep.c_dtype == kF32 && (ep.ldc % 4) == 0 &&
+      (ep.resid == nullptr || (ep.ld_resid % 4) == 0)) {
+    float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(ep.C) + (size_t)m * ep.ldc + nb);
+    const float4* res = ep.resid ? reinterpret_cast<const float4*>(ep.resid + (size_t)m * ep.ld_resid + nb)
+                                 : nullptr;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      float4 o;
+      o.x = v[4 * i] + bs[4 * i];
+      o.y = v[4 * i + 1] + bs[4 * i + 1];
+      o.z = v[4 * i + 2] + bs[4 * i + 2];
+      o.w = v[4 * i + 3] + bs[4 * i + 3];
+      if (res) {
+        const float4 r = res[i];
+        o.x = r.x + o.x;
+        o.y = r.y + o.y;
+        o.z = r.z + o.z;
+        o.w = r.w + o.w;
+      }
+      if (ep.relu) {
+        o.x = fmaxf(o.x, 0.f);
+        o.y = fmaxf(o.y, 0.f);
+        o.z = fmaxf(o.z, 0.f);
+        o.w = fmaxf(o.w, 0.f);
+      }
+      dst[i] = o;
+    }
+    return;
+  }
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const int n = nb + i;
+    if (n < ep.N) {
+      float x = v[i] + bs[i];
+      if (ep.resid) x = ep.resid[(size_t)m * ep.ld_resid + n] + x;
+      if (ep.relu) x = fmaxf(x, 0.f);
+      store_elem(ep, m, n, x);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// persistent tcgen05 kernel
+
+template <int BN, int STAGES>
+struct TcCfg {
+  static constexpr int kBBytes = BN * kBK * 2;
+  static constexpr int kStage = kABytes + kBBytes;
+  static constexpr int kTmemCols = 2 * BN;   // double-buffered accumulator
+  static constexpr int kSmem = 1024 + STAGES * kStage + 2 * BN * 4 + 256;
+};
+
+constexpr int kTcThreads = 192;
+
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(kTcThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmw,
-                   int K, uint32_t idesc, EpiParams ep) {
+                   int K, uint32_t idesc, EpiParams ep, int tiles_n, int tiles) {
+  using Cfg = TcCfg<BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
   uint8_t* sA = base;
-  uint8_t* sB = base + kStages * kABytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + kStages * kBBytes);
-  uint64_t* empty = full + kStages;
-  uint64_t* done = empty + kStages;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
+  uint8_t* sB = base + STAGES * kABytes;
+  float* bias_s = reinterpret_cast<float*>(sB + STAGES * Cfg::kBBytes);   // [2][BN]
+  uint64_t* full = reinterpret_cast<uint64_t*>(bias_s + 2 * BN);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int n0 = blockIdx.x * kBN;
-  const int m0 = blockIdx.y * kBM;
   const int nk = (K + kBK - 1) / kBK;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tma);
     tma_prefetch_desc(&tmw);
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < STAGES; ++s) {
       mbar_init(full + s, 1);
       mbar_init(empty + s, 1);
     }
-    mbar_init(done, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(tfull + b, 1);
+      mbar_init(tempty + b, 4);
+    }
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc(tslot, kBN);
+  if (warp == 1) tmem_alloc(tslot, Cfg::kTmemCols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
 
-  if (warp == 0 && lane == 0) {
-    // TMA producer
-    for (int kb = 0; kb < nk; ++kb) {
-      const int s = kb % kStages;
-      const uint32_t ph = (kb / kStages) & 1;
-      mbar_wait(empty + s, ph ^ 1);
-      mbar_expect_tx(full + s, kABytes + kBBytes);
-      tma_load_2d(sA + s * kABytes, &tma, full + s, kb * kBK, m0);
-      tma_load_2d(sB + s * kBBytes, &tmw, full + s, kb * kBK, n0);
+  if (warp == 0) {
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        const int m0 = (tile / tiles_n) * kBM;
+        const int n0 = (tile % tiles_n) * BN;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(empty + s, ph ^ 1);
+          mbar_expect_tx(full + s, Cfg::kStage);
+          tma_load_2d(sA + s * kABytes, &tma, full + s, kb * kBK, m0);
+#pragma unroll
+          for (int j = 0; j < BN / kWBox; ++j)
+            tma_load_2d(sB + s * Cfg::kBBytes + j * kWBox * 128, &tmw, full + s, kb * kBK,
+                        n0 + j * kWBox);
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
     }
-  } else if (warp == 1 && lane == 0) {
-    // MMA issuer (single thread)
-    for (int kb = 0; kb < nk; ++kb) {
-      const int s = kb % kStages;
-      const uint32_t ph = (kb / kStages) & 1;
-      mbar_wait(full + s, ph);
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      int acc = 0;
+      uint32_t aph = 0;
+      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        mbar_wait(tempty + acc, aph ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + acc * BN;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(full + s, ph);
+          tc_fence_after();
+          const uint64_t ad = umma_desc_sw128(smem_u32(sA + s * kABytes));
+          const uint64_t bd = umma_desc_sw128(smem_u32(sB + s * Cfg::kBBytes));
+#pragma unroll
+          for (int kk = 0; kk < kBK / 16; ++kk)
+            tc_mma_f16(d, ad + 2 * kk, bd + 2 * kk, idesc, (kb | kk) != 0 ? 1u : 0u);
+          tc_commit(empty + s);
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+        tc_commit(tfull + acc);
+        acc ^= 1;
+        if (acc == 0) aph ^= 1;
+      }
+    }
+  } else {
+    // epilogue warps 2..5: TMEM lane quarter = warp % 4
+    const int quarter = warp & 3;
+    int acc = 0;
+    uint32_t aph = 0;
+    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+      const int m0 = (tile / tiles_n) * kBM;
+      const int n0 = (tile % tiles_n) * BN;
+      // stage this tile's bias while the MMAs run (double-buffered by acc)
+      float* bs = bias_s + acc * BN;
+      for (int i = threadIdx.x - 64; i < BN; i += 128)
+        bs[i] = (ep.bias && n0 + i < ep.N) ? ep.bias[n0 + i] : 0.f;
+      named_bar_sync(1, 128);
+      mbar_wait(tfull + acc, aph);
       tc_fence_after();
-      const uint64_t ad = umma_desc_sw128(smem_u32(sA + s * kABytes));
-      const uint64_t bd = umma_desc_sw128(smem_u32(sB + s * kBBytes));
-#pragma unroll
-      for (int kk = 0; kk < kBK / 16; ++kk)
-        tc_mma_f16(tmem, ad + 2 * kk, bd + 2 * kk, idesc, (kb | kk) != 0 ? 1u : 0u);
-      tc_commit(empty + s);
-    }
-    tc_commit(done);
-  }
-  __syncwarp();
-  mbar_wait(done, 0);
-  tc_fence_after();
-
-  // Epilogue: warp w owns TMEM lanes [32w, 32w+32) == tile rows.
-  const int m = m0 + warp * 32 + lane;
-  const bool row_ok = m < ep.M;
-  const uint32_t lane_addr = tmem + ((uint32_t)(warp * 32) << 16);
-  unsigned long long best = 0ull;
+      const int m = m0 + quarter * 32 + lane;
+      const bool row_ok = m < ep.M;
+      const uint32_t taddr = tmem + acc * BN + ((uint32_t)(quarter * 32) << 16);
+      float best_v = -INFINITY;
+      int best_i = -1;
 #pragma unroll 1
-  for (int c = 0; c < kBN / 32; ++c) {
-    float v[32];
-    tmem_ld32(lane_addr + c * 32, v);
-    const int nb = n0 + c * 32;
-    if (!row_ok || nb >= ep.N) continue;
-    if (ep.epi == kEpiArgmax) {
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const int n = nb + i;
-        if (n < ep.N) {
-          unsigned long long key = argmax_key(v[i] + ep.bias[n], (uint32_t)n);
-          best = key > best ? key : best;
-        }
+      for (int c = 0; c < BN / 32; ++c) {
+        float v[32];
+        tmem_ld32(taddr + c * 32, v);
+        const int nb = n0 + c * 32;
+        if (row_ok && nb < ep.N) epilogue_chunk(ep, m, nb, v, bs + c * 32, best_v, best_i);
       }
-      continue;
-    }
-    const bool full_chunk = nb + 32 <= ep.N;
-    if (full_chunk && ep.c_dtype != kF32 && (ep.ldc % 8) == 0 && ep.resid == nullptr) {
-      uint32_t packed[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        float a = v[2 * i] + (ep.bias ? ep.bias[nb + 2 * i] : 0.f);
-        float b = v[2 * i + 1] + (ep.bias ? ep.bias[nb + 2 * i + 1] : 0.f);
-        if (ep.relu) {
-          a = fmaxf(a, 0.f);
-          b = fmaxf(b, 0.f);
-        }
-        if (ep.c_dtype == kF16) {
-          __half2 h = __floats2half2_rn(a, b);
-          packed[i] = *reinterpret_cast<uint32_t*>(&h);
-        } else {
-          __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
-          packed[i] = *reinterpret_cast<uint32_t*>(&h);
-        }
-      }
-      uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(ep.C) +
-                                            (size_t)m * ep.ldc + nb);
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-        dst[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
-    } else {
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const int n = nb + i;
-        if (n < ep.N) store_elem(ep, m, n, epi_value(ep, m, n, v[i]));
-      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty + acc);
+      if (ep.epi == kEpiArgmax && row_ok && best_i >= 0)
+        atomicMax(ep.keys + m, argmax_key(best_v, (uint32_t)best_i));
+      acc ^= 1;
+      if (acc == 0) aph ^= 1;
     }
   }
-  if (ep.epi == kEpiArgmax && row_ok && best != 0ull) atomicMax(ep.keys + m, best);
-
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc(tmem, kBN);
+  if (warp == 1) tmem_dealloc(tmem, Cfg::kTmemCols);
 }
 
 // ---------------------------------------------------------------------------
@@ -267,9 +380,40 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <int BN, int STAGES>
+cudaError_t launch_tc(const CUtensorMap& ta, const CUtensorMap& tw, const GemmArgs& g,
+                      const EpiParams& ep, cudaStream_t s) {
+  using Cfg = TcCfg<BN, STAGES>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<BN, STAGES>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int tiles_n = (g.N + BN - 1) / BN;
+  const int tiles = tiles_n * ((g.M + kBM - 1) / kBM);
+  const int grid = tiles < num_sms() ? tiles : num_sms();
+  const uint32_t idesc = umma_idesc_f16(kBM, BN, g.in_dtype == kBF16);
+  gemm_tc_kernel<BN, STAGES><<<grid, kTcThreads, Cfg::kSmem, s>>>(ta, tw, g.K, idesc, ep,
+                                                                  tiles_n, tiles);
+  return cudaGetLastError();
+}
+
 }  // namespace
 
-int gemm_tile_n() { return kBN; }
+int gemm_tile_n() { return kWBox; }
 
 bool make_tmap_16(CUtensorMap* out, const void* base, int dtype, int64_t rows, int64_t cols,
                   int64_t ld, int box_rows, std::string* err) {
@@ -297,6 +441,16 @@ bool make_tmap_16(CUtensorMap* out, const void* base, int dtype, int64_t rows, i
   return true;
 }
 
+// N tile: the largest of 256/128/64 that still gives about one wave of tiles.
+int pick_bn(int M, int N) {
+  const int mt = (M + kBM - 1) / kBM;
+  const int sms = num_sms();
+  for (int bn : {256, 128}) {
+    if ((int64_t)mt * ((N + bn - 1) / bn) >= sms) return bn;
+  }
+  return 64;
+}
+
 cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t s) {
   if (g.M <= 0 || g.N <= 0) return cudaSuccess;
   EpiParams ep{g.bias, g.M, g.N, g.epi, g.C, g.ldc, g.c_dtype, g.relu, g.resid, g.ld_resid, g.keys};
@@ -315,21 +469,15 @@ cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t s) {
     pa = &ta;
   }
   if (!pw) {
-    if (!make_tmap_16(&tw, g.W, g.in_dtype, g.N, g.K, g.ldw, kBN, nullptr))
+    if (!make_tmap_16(&tw, g.W, g.in_dtype, g.N, g.K, g.ldw, kWBox, nullptr))
       return cudaErrorInvalidValue;
     pw = &tw;
   }
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         kTcSmem);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
+  switch (pick_bn(g.M, g.N)) {
+    case 256: return launch_tc<256, 4>(*pa, *pw, g, ep, s);
+    case 128: return launch_tc<128, 6>(*pa, *pw, g, ep, s);
+    default: return launch_tc<64, 8>(*pa, *pw, g, ep, s);
   }
-  dim3 grid((g.N + kBN - 1) / kBN, (g.M + kBM - 1) / kBM);
-  const uint32_t idesc = umma_idesc_f16(kBM, kBN, g.in_dtype == kBF16);
-  gemm_tc_kernel<<<grid, 128, kTcSmem, s>>>(*pa, *pw, g.K, idesc, ep);
-  return cudaGetLastError();
 }
 
 }  // namespace fnmt

@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--profile-sentences", type=int, default=16384)
+    ap.add_argument("--wbatch", type=int, default=64000, help="token cap (paper GPU setting 64000)")
+    ap.add_argument("--sbatch", type=int, default=3072, help="sentence cap (paper GPU setting 3072)")
     return ap.parse_args()
 
 
@@ -245,7 +247,9 @@ def run_reference(args):
 # ----------------------------------------------------------------------------
 
 def main():
+    global SBATCH, WBATCH
     args = parse()
+    SBATCH, WBATCH = args.sbatch, args.wbatch
     if args.impl == "reference":
         return run_reference(args)
     import torch

@@ -262,8 +262,10 @@ __device__ __forceinline__ void softmax_inplace(float* S, int nk) {
 }
 
 // G lanes cooperate on one key (CH 16-byte chunks each); 32/G keys per warp.
-template <typename T, int G, int CH>
-__global__ void __launch_bounds__(kDThreads) attn_decode_kernel(DecAttnArgs a, float qscale) {
+// NT threads per (row, head): 128 normally, 512 when there are too few rows
+// to fill the machine (long-sentence batches).
+template <typename T, int G, int CH, int NT>
+__global__ void __launch_bounds__(NT) attn_decode_kernel(DecAttnArgs a, float qscale) {
   constexpr int VEC = Vec16<T>::N;
   extern __shared__ float sm[];
   const int dk = a.dk;
@@ -274,31 +276,46 @@ __global__ void __launch_bounds__(kDThreads) attn_decode_kernel(DecAttnArgs a, f
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const DecCtx c = decode_setup<T>(a, r, h);
   const T* q = reinterpret_cast<const T*>(a.q) + (size_t)r * a.ldq + h * dk;
-  for (int e = tid; e < dk; e += kDThreads) qs[e] = to_f32(q[e]) * qscale;
+  for (int e = tid; e < dk; e += NT) qs[e] = to_f32(q[e]) * qscale;
   __syncthreads();
 
   const T* kb = reinterpret_cast<const T*>(a.k) + h * dk;
-  constexpr int KPW = 32 / G;
+  constexpr int KPW = 32 / G;            // keys per warp per round (lane groups)
+  constexpr int U = 1;                   // rounds unrolled: U * KPW keys in flight per warp
   const int g = lane / G, li = lane % G;
-  for (int j0 = warp * KPW; j0 < c.nk; j0 += (kDThreads / 32) * KPW) {
-    const int j = j0 + g;
-    float s = 0.f;
-    if (j < c.nk) {
-      const T* kr = kb + decode_key_row(a, c, r, j) * a.ldkv;
+  const int stride = (NT / 32) * KPW;
+  for (int j0 = warp * KPW; j0 < c.nk; j0 += stride * U) {
+    float f[U][CH][VEC];
 #pragma unroll
-      for (int ch = 0; ch < CH; ++ch) {
-        const int e0 = (li + ch * G) * VEC;
-        if (e0 < dk) {
-          float f[VEC];
-          load16(kr + e0, f);
+    for (int u = 0; u < U; ++u) {
+      const int j = j0 + u * stride + g;
+      if (j < c.nk) {
+        const T* kr = kb + decode_key_row(a, c, r, j) * a.ldkv;
 #pragma unroll
-          for (int i = 0; i < VEC; ++i) s = fmaf(qs[e0 + i], f[i], s);
+        for (int ch = 0; ch < CH; ++ch) {
+          const int e0 = (li + ch * G) * VEC;
+          if (e0 < dk) load16(kr + e0, f[u][ch]);
         }
       }
     }
 #pragma unroll
-    for (int o = G / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (li == 0 && j < c.nk) S[j] = c.all_masked ? s + kMaskValue : s;
+    for (int u = 0; u < U; ++u) {
+      const int j = j0 + u * stride + g;
+      float s = 0.f;
+      if (j < c.nk) {
+#pragma unroll
+        for (int ch = 0; ch < CH; ++ch) {
+          const int e0 = (li + ch * G) * VEC;
+          if (e0 < dk) {
+#pragma unroll
+            for (int i = 0; i < VEC; ++i) s = fmaf(qs[e0 + i], f[u][ch][i], s);
+          }
+        }
+      }
+#pragma unroll
+      for (int o = G / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (li == 0 && j < c.nk) S[j] = c.all_masked ? s + kMaskValue : s;
+    }
   }
   __syncthreads();
   if (warp == 0) softmax_inplace(S, c.nk);
@@ -306,26 +323,40 @@ __global__ void __launch_bounds__(kDThreads) attn_decode_kernel(DecAttnArgs a, f
 
   // value product: thread = (chunk, key group)
   const int nch = dk / VEC;
-  const int groups = kDThreads / nch;
+  const int groups = NT / nch;
   const int ch = tid % nch, grp = tid / nch;
   const T* vb = reinterpret_cast<const T*>(a.v) + h * dk + ch * VEC;
   float acc[VEC];
 #pragma unroll
   for (int i = 0; i < VEC; ++i) acc[i] = 0.f;
   if (grp < groups) {
-    for (int j = grp; j < c.nk; j += groups) {
-      float f[VEC];
-      load16(vb + decode_key_row(a, c, r, j) * a.ldkv, f);
-      const float w = S[j];
+    constexpr int U3 = 1;   // value rows in flight per thread
+    for (int j0 = grp; j0 < c.nk; j0 += groups * U3) {
+      float f[U3][VEC];
+      float w[U3];
 #pragma unroll
-      for (int i = 0; i < VEC; ++i) acc[i] = fmaf(w, f[i], acc[i]);
+      for (int u = 0; u < U3; ++u) {
+        const int j = j0 + u * groups;
+        if (j < c.nk) {
+          load16(vb + decode_key_row(a, c, r, j) * a.ldkv, f[u]);
+          w[u] = S[j];
+        } else {
+          w[u] = 0.f;
+#pragma unroll
+          for (int i = 0; i < VEC; ++i) f[u][i] = 0.f;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U3; ++u)
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) acc[i] = fmaf(w[u], f[u][i], acc[i]);
     }
 #pragma unroll
     for (int i = 0; i < VEC; ++i) red[grp * dk + ch * VEC + i] = acc[i];
   }
   __syncthreads();
   T* out = reinterpret_cast<T*>(a.out) + (size_t)r * a.ldo + h * dk;
-  for (int e = tid; e < dk; e += kDThreads) {
+  for (int e = tid; e < dk; e += NT) {
     float sum = red[e];
     for (int gg = 1; gg < groups; ++gg) sum += red[gg * dk + e];
     out[e] = from_f32<T>(sum);
@@ -383,15 +414,25 @@ cudaError_t varlen_dispatch(const AttnArgs& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-template <typename T, int G, int CH>
-cudaError_t launch_dec(const DecAttnArgs& a, float qscale, size_t smem, cudaStream_t s) {
+template <typename T, int G, int CH, int NT>
+cudaError_t launch_dec_nt(const DecAttnArgs& a, float qscale, cudaStream_t s) {
+  const int groups = NT / (a.dk / Vec16<T>::N);
+  const size_t smem = sizeof(float) * ((size_t)a.dk + a.max_k + 4 + (size_t)groups * a.dk);
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(attn_decode_kernel<T, G, CH>,
+    cudaError_t e = cudaFuncSetAttribute(attn_decode_kernel<T, G, CH, NT>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  attn_decode_kernel<T, G, CH><<<dim3(a.rows, a.heads), kDThreads, smem, s>>>(a, qscale);
+  attn_decode_kernel<T, G, CH, NT><<<dim3(a.rows, a.heads), NT, smem, s>>>(a, qscale);
   return cudaGetLastError();
+}
+
+template <typename T, int G, int CH>
+cudaError_t launch_dec(const DecAttnArgs& a, float qscale, cudaStream_t s) {
+  // few (row, head) blocks -> wide blocks so the SMs still have enough warps in flight
+  if ((int64_t)a.rows * a.heads < 1200) return launch_dec_nt<T, G, CH, 512>(a, qscale, s);
+  return launch_dec_nt<T, G, CH, 128>(a, qscale, s);
 }
 
 template <typename T>
@@ -399,21 +440,18 @@ cudaError_t decode_dispatch(const DecAttnArgs& a, cudaStream_t s) {
   constexpr int VEC = Vec16<T>::N;
   const float qscale = (float)(1.0 / sqrt((double)a.dk));
   const int nch = a.dk / VEC;
-  const bool vec_ok = a.dk % VEC == 0 && nch <= kDThreads && (a.ldkv % VEC) == 0;
+  const bool vec_ok = a.dk % VEC == 0 && nch <= kDThreads && (a.ldkv % VEC) == 0 &&
+                      sizeof(float) * ((size_t)a.dk * 5 + a.max_k + 4) <= 227 * 1024;
   if (vec_ok) {
-    const int groups = kDThreads / nch;
-    const size_t smem = sizeof(float) * ((size_t)a.dk + a.max_k + 4 + (size_t)groups * a.dk);
-    if (smem <= 227 * 1024) {
-      if (nch <= 1) return launch_dec<T, 1, 1>(a, qscale, smem, s);
-      if (nch <= 2) return launch_dec<T, 2, 1>(a, qscale, smem, s);
-      if (nch <= 4) return launch_dec<T, 4, 1>(a, qscale, smem, s);
-      if (nch <= 8) return launch_dec<T, 8, 1>(a, qscale, smem, s);
-      if (nch <= 16) return launch_dec<T, 16, 1>(a, qscale, smem, s);
-      if (nch <= 32) return launch_dec<T, 32, 1>(a, qscale, smem, s);
-      if (nch <= 64) return launch_dec<T, 32, 2>(a, qscale, smem, s);
-      if (nch <= 96) return launch_dec<T, 32, 3>(a, qscale, smem, s);
-      return launch_dec<T, 32, 4>(a, qscale, smem, s);
-    }
+    if (nch <= 1) return launch_dec<T, 1, 1>(a, qscale, s);
+    if (nch <= 2) return launch_dec<T, 2, 1>(a, qscale, s);
+    if (nch <= 4) return launch_dec<T, 4, 1>(a, qscale, s);
+    if (nch <= 8) return launch_dec<T, 8, 1>(a, qscale, s);
+    if (nch <= 16) return launch_dec<T, 16, 1>(a, qscale, s);
+    if (nch <= 32) return launch_dec<T, 32, 1>(a, qscale, s);
+    if (nch <= 64) return launch_dec<T, 32, 2>(a, qscale, s);
+    if (nch <= 96) return launch_dec<T, 32, 3>(a, qscale, s);
+    return launch_dec<T, 32, 4>(a, qscale, s);
   }
   const size_t smem = sizeof(float) * ((size_t)a.dk + (size_t)a.max_k + 32);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;

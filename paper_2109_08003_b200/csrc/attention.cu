@@ -240,7 +240,10 @@ __device__ __forceinline__ DecCtx decode_setup(const DecAttnArgs& a, int r, int 
 __device__ __forceinline__ int64_t decode_key_row(const DecAttnArgs& a, const DecCtx& c, int r,
                                                   int j) {
   if (a.self_mode) {
-    const int src = (a.anc && j < c.t) ? a.anc[(size_t)r * a.cap + j] : r;
+    // beam: key j of row r was written by cache row anc_t[r][j] (table for step parity t & 1)
+    const int src = (a.anc && j < c.t)
+                        ? a.anc[(size_t)(c.t & 1) * a.anc_buf_stride + (size_t)r * a.cap + j]
+                        : r;
     return (int64_t)src * a.cap + j;
   }
   return c.seq_row0 + j;

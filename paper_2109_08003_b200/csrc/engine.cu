@@ -636,6 +636,7 @@ void Engine::run_step(const StepView& v, cudaStream_t s) {
     a.cap = v.cap;
     a.t_ptr = v.t_ptr;
     a.anc = v.anc;
+    a.anc_buf_stride = v.anc_stride;
     a.max_k = v.cap;
     {
       const int ev = prof_begin(s);
@@ -678,8 +679,34 @@ void Engine::run_step(const StepView& v, cudaStream_t s) {
       norm(ws.dx32, ws.dy32, L.n3, ws.dx32, ws.dxa, R, s);
     }
   }
-  if (v.logits) {
+  if (v.topk && tc) {
+    // beam: vocab projection fused with per-tile max / sum-exp / top-K
+    GemmArgs g;
+    g.A = ws.dxa;
+    g.lda = d;
+    g.W = out.w;
+    g.ldw = out.K;
+    g.in_dtype = dt;
+    g.bias = out.b;
+    g.M = R;
+    g.N = out.N;
+    g.K = out.K;
+    g.epi = kEpiTopK;
+    g.topk = *v.topk;
+    g.tmap_a = &ws.tm_dxa;
+    g.tmap_w = &out.tm;
+    const int ev = prof_begin(s);
+    CK(launch_gemm(g, s));
+    prof_end(s, ev, FNMT_K_VOCAB, 2.0 * R * out.N * out.K,
+             (double)R * out.K * dtype_size(dt) + (double)out.N * out.K * dtype_size(dt));
+    ++launches;
+  } else if (v.logits) {
+    gemm_cls = FNMT_K_VOCAB;
     gemm(ws.dxa, tc ? &ws.tm_dxa : nullptr, d, out, R, v.logits, arch.vocab_size, kF32, 0, s);
+    if (v.topk) {
+      CK(launch_logits_topk_partials(v.logits, R, arch.vocab_size, *v.topk, s));
+      ++launches;
+    }
   } else {
     gemm_argmax(ws.dxa, tc ? &ws.tm_dxa : nullptr, d, R, v.keys, s);
   }
@@ -695,9 +722,10 @@ void Engine::translate_device(const int32_t* d_ids, const int64_t* d_off,
                               int32_t* d_out_ids, const int64_t* d_out_off, int32_t* d_out_len,
                               fnmt_stats* st) {
   if (!finalized) throw EngineError(FNMT_E_STATE, "engine not finalized");
-  if (run.beam_size != 1)
-    throw EngineError(FNMT_E_INVALID, "corpus translate: only greedy (beam_size 1) is implemented");
+  if (run.beam_size < 1 || run.beam_size > kTopKMax)
+    throw EngineError(FNMT_E_INVALID, "beam_size must be in [1, 8]");
   if (run.sbatch < 1 || run.wbatch < 1) throw EngineError(FNMT_E_INVALID, "sbatch/wbatch must be >= 1");
+  const int kb = run.beam_size;
   CK(cudaSetDevice(device));
   const int n = (int)lengths.size();
   for (int32_t L : lengths) {
@@ -752,7 +780,8 @@ void Engine::translate_device(const int32_t* d_ids, const int64_t* d_off,
       rows_need = std::max(rows_need, R);
       pool_need = std::max<int64_t>(pool_need, (int64_t)R * cap);
     }
-    reserve(tok_need, rows_need, pool_need);
+    reserve(tok_need, rows_need * kb, pool_need * kb);
+    if (kb > 1) reserve_beam(rows_need, kb, pool_need * kb);
   }
   ensure_meta(perm.size(), cu_all.size());
   if (!perm.empty()) {
@@ -797,75 +826,19 @@ void Engine::translate_device(const int32_t* d_ids, const int64_t* d_off,
     ++launches;
     encoder_layers(n_tok, R, b.max_len, b.max_len, ws.cu, ws.len, ws.cu, ws.len, 0, stream);
     cross_kv_all(n_tok, stream);
-    // 3) greedy decode, one CUDA graph per step
-    init_decode_kernel<<<(R + 255) / 256, 256, 0, stream>>>(ws.prev, ws.finished, ws.out_len,
-                                                           ws.keys, ws.t, ws.alive, R, run.bos_id);
-    CK(cudaGetLastError());
-    ++launches;
-    StepView v;
-    v.rows = R;
-    v.cap = cap;
-    v.prev = ws.prev;
-    v.t_ptr = ws.t;
-    v.kc = ws.kc.data();
-    v.vc = ws.vc.data();
-    v.ckv = (const void* const*)ws.ckv.data();
-    v.k_start = ws.cu;
-    v.k_len = ws.len;
-    v.k_pad = 0;
-    v.rows_per_seq = 1;
-    v.max_k = b.max_len;
-    v.keys = ws.keys;
-    GreedyState gs;
-    gs.keys = ws.keys;
-    gs.prev = ws.prev;
-    gs.finished = ws.finished;
-    gs.budget = ws.budget;
-    gs.out_ids = ws.out_ids;
-    gs.out_len = ws.out_len;
-    gs.t = ws.t;
-    gs.alive = ws.alive;
-    gs.rows = R;
-    gs.out_cap = cap;
-    gs.eos = run.eos_id;
-    gs.pad = run.pad_id;
-    const int64_t nodes = profiling ? 0 : capture_step(v, gs);
-    const int chunk = 8;
-    int steps = 0;
-    int inflight = 0;
-    bool stop = false;
-    for (int c0 = 0; c0 < cap && !stop; c0 += chunk) {
-      const int c1 = std::min(cap, c0 + chunk);
-      if (profiling) {
-        // un-captured launches so every kernel can be bracketed by events
-        for (int t = c0; t < c1; ++t) {
-          v.host_t = t;
-          run_step(v, stream);
-          const int ev = prof_begin(stream);
-          CK(launch_greedy_update(gs, stream));
-          prof_end(stream, ev, FNMT_K_SEARCH, 0.0, (double)R * 24);
-          ++launches;
-        }
-      } else {
-        for (int t = c0; t < c1; ++t) CK(cudaGraphLaunch(graph_exec, stream));
-        launches += nodes * (c1 - c0);
-      }
-      steps += c1 - c0;
-      const int slot = (c0 / chunk) & 1;
-      if (inflight == 2) {
-        // wait for the chunk before the previous one; stop when every row finished
-        CK(cudaEventSynchronize(ev_poll[slot]));
-        if (h_alive[slot] == 0) stop = true;
-        --inflight;
-      }
-      CK(cudaMemcpyAsync(h_alive + slot, ws.alive, sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
-      CK(cudaEventRecord(ev_poll[slot], stream));
-      ++inflight;
+    // 3) decode: one CUDA graph per step (greedy, or batched beam)
+    const int32_t* res_ids = ws.out_ids;
+    const int32_t* res_len = ws.out_len;
+    if (run.beam_size <= 1) {
+      steps_total += decode_greedy(R, cap, b.max_len, run);
+    } else {
+      steps_total += decode_beam(R, cap, b.max_len, run);
+      res_ids = beam.out_ids;
+      res_len = beam.out_len;
     }
-    steps_total += steps;
     // 4) restore order: scatter rows to their sentence slots
     ev = prof_begin(stream);
-    scatter_out_kernel<<<R, 64, 0, stream>>>(ws.out_ids, ws.out_len, cap, perm_b, R, d_out_off,
+    scatter_out_kernel<<<R, 64, 0, stream>>>(res_ids, res_len, cap, perm_b, R, d_out_off,
                                             d_out_ids, d_out_len);
     CK(cudaGetLastError());
     prof_end(stream, ev, FNMT_K_OTHER, 0.0, (double)R * cap * 8);
@@ -890,6 +863,198 @@ void Engine::translate_device(const int32_t* d_ids, const int64_t* d_off,
   }
 }
 
+// Replay the captured step (or, when profiling, launch `direct(t)`) for up to
+// `cap` steps; every 8 steps the device `alive` count is copied back and the
+// loop stops once it reads zero (checked two chunks behind, so the host
+// never waits on the chunk it just queued).
+int Engine::drive_steps(int cap, int64_t nodes, const std::function<void(int)>& direct) {
+  const int chunk = 8;
+  int steps = 0, inflight = 0;
+  bool stop = false;
+  for (int c0 = 0; c0 < cap && !stop; c0 += chunk) {
+    const int c1 = std::min(cap, c0 + chunk);
+    if (profiling) {
+      for (int t = c0; t < c1; ++t) direct(t);
+    } else {
+      for (int t = c0; t < c1; ++t) CK(cudaGraphLaunch(graph_exec, stream));
+      launches += nodes * (c1 - c0);
+    }
+    steps += c1 - c0;
+    const int slot = (c0 / chunk) & 1;
+    if (inflight == 2) {
+      CK(cudaEventSynchronize(ev_poll[slot]));
+      if (h_alive[slot] == 0) stop = true;
+      --inflight;
+    }
+    CK(cudaMemcpyAsync(h_alive + slot, ws.alive, sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
+    CK(cudaEventRecord(ev_poll[slot], stream));
+    ++inflight;
+  }
+  return steps;
+}
+
+StepView Engine::step_view(int rows, int cap, int max_len, int rows_per_seq) {
+  StepView v;
+  v.rows = rows;
+  v.cap = cap;
+  v.prev = ws.prev;
+  v.t_ptr = ws.t;
+  v.kc = ws.kc.data();
+  v.vc = ws.vc.data();
+  v.ckv = (const void* const*)ws.ckv.data();
+  v.k_start = ws.cu;
+  v.k_len = ws.len;
+  v.k_pad = 0;
+  v.rows_per_seq = rows_per_seq;
+  v.max_k = max_len;
+  return v;
+}
+
+int Engine::decode_greedy(int R, int cap, int max_len, const fnmt_run& run) {
+  init_decode_kernel<<<(R + 255) / 256, 256, 0, stream>>>(ws.prev, ws.finished, ws.out_len,
+                                                         ws.keys, ws.t, ws.alive, R, run.bos_id);
+  CK(cudaGetLastError());
+  ++launches;
+  StepView v = step_view(R, cap, max_len, 1);
+  v.keys = ws.keys;
+  GreedyState gs;
+  gs.keys = ws.keys;
+  gs.prev = ws.prev;
+  gs.finished = ws.finished;
+  gs.budget = ws.budget;
+  gs.out_ids = ws.out_ids;
+  gs.out_len = ws.out_len;
+  gs.t = ws.t;
+  gs.alive = ws.alive;
+  gs.rows = R;
+  gs.out_cap = cap;
+  gs.eos = run.eos_id;
+  gs.pad = run.pad_id;
+  auto body = [&](int t) {
+    v.host_t = t;
+    run_step(v, stream);
+    const int ev = prof_begin(stream);
+    CK(launch_greedy_update(gs, stream));
+    prof_end(stream, ev, FNMT_K_SEARCH, 0.0, (double)R * 24);
+    ++launches;
+  };
+  const int64_t nodes = profiling ? 0 : capture_step([&] { body(0); });
+  return drive_steps(cap, nodes, body);
+}
+
+void Engine::reserve_beam(int sent_cap, int k, int64_t pool_cap) {
+  const int rows = sent_cap * k;
+  const int tiles = (arch.vocab_size + kTopKTile - 1) / kTopKTile;
+  const int K = k <= 4 ? 4 : 8;
+  if (beam.owned.size() && sent_cap <= beam.sent_cap && k <= beam.k && pool_cap <= beam.pool_cap &&
+      K <= beam.part.K)
+    return;
+  CK(cudaStreamSynchronize(stream));
+  for (void* p : beam.owned) {
+    cudaFree(p);
+    allocations.erase(std::find(allocations.begin(), allocations.end(), p));
+  }
+  device_bytes -= beam.bytes;
+  beam = BeamWs();
+  const int64_t before = device_bytes;
+  auto alloc = [&](size_t bytes) {
+    void* p = dalloc(bytes);
+    beam.owned.push_back(p);
+    return p;
+  };
+  beam.sent_cap = sent_cap;
+  beam.k = k;
+  beam.pool_cap = pool_cap;
+  const int64_t cap_per_row = pool_cap / rows + 1;
+  beam.part.tiles = tiles;
+  beam.part.K = K;
+  beam.part.pmax = (float*)alloc(sizeof(float) * (size_t)rows * tiles);
+  beam.part.psum = (double*)alloc(sizeof(double) * (size_t)rows * tiles);
+  beam.part.pval = (float*)alloc(sizeof(float) * (size_t)rows * tiles * K);
+  beam.part.pidx = (int32_t*)alloc(sizeof(int32_t) * (size_t)rows * tiles * K);
+  beam.rval = (float*)alloc(sizeof(float) * (size_t)rows * k);
+  beam.ridx = (int32_t*)alloc(sizeof(int32_t) * (size_t)rows * k);
+  beam.rlogz = (double*)alloc(sizeof(double) * rows);
+  beam.score = (double*)alloc(sizeof(double) * rows);
+  beam.active = (uint8_t*)alloc(rows);
+  beam.anc = (int32_t*)alloc(sizeof(int32_t) * 2 * (size_t)pool_cap);
+  beam.tok_hist = (int32_t*)alloc(sizeof(int32_t) * (size_t)pool_cap);
+  beam.par_hist = (int32_t*)alloc(sizeof(int32_t) * (size_t)pool_cap);
+  beam.finished = (uint8_t*)alloc(sent_cap);
+  beam.n_done = (int32_t*)alloc(sizeof(int32_t) * sent_cap);
+  beam.fin_t = (int32_t*)alloc(sizeof(int32_t) * sent_cap);
+  beam.fin_n = (int32_t*)alloc(sizeof(int32_t) * sent_cap);
+  beam.done_score = (double*)alloc(sizeof(double) * sent_cap * 2 * k);
+  beam.done_t = (int32_t*)alloc(sizeof(int32_t) * sent_cap * 2 * k);
+  beam.done_slot = (int32_t*)alloc(sizeof(int32_t) * sent_cap * 2 * k);
+  beam.ticket = (uint32_t*)alloc(sizeof(uint32_t) * 2);
+  // per batch: R sentences x cap steps <= pool_cap / k (the plan's max R * cap)
+  (void)cap_per_row;
+  beam.out_ids = (int32_t*)alloc(sizeof(int32_t) * (size_t)(pool_cap / k + 1));
+  beam.out_len = (int32_t*)alloc(sizeof(int32_t) * sent_cap);
+  beam.scratch = (int32_t*)alloc(sizeof(int32_t) * (size_t)(2 * pool_cap + 1));
+  if (dt == kF32) beam.logits = (float*)alloc(sizeof(float) * (size_t)rows * arch.vocab_size);
+  beam.bytes = device_bytes - before;
+}
+
+int Engine::decode_beam(int R, int cap, int max_len, const fnmt_run& run) {
+  const int k = run.beam_size;
+  const int rows = R * k;
+  BeamState bs;
+  bs.nS = R;
+  bs.k = k;
+  bs.cap = cap;
+  bs.rows = rows;
+  bs.eos = run.eos_id;
+  bs.pad = run.pad_id;
+  bs.part = beam.part;
+  bs.rval = beam.rval;
+  bs.ridx = beam.ridx;
+  bs.rlogz = beam.rlogz;
+  bs.prev = ws.prev;
+  bs.score = beam.score;
+  bs.active = beam.active;
+  bs.anc = beam.anc;
+  bs.tok_hist = beam.tok_hist;
+  bs.par_hist = beam.par_hist;
+  bs.budget = ws.budget;
+  bs.finished = beam.finished;
+  bs.n_done = beam.n_done;
+  bs.done_score = beam.done_score;
+  bs.done_t = beam.done_t;
+  bs.done_slot = beam.done_slot;
+  bs.fin_t = beam.fin_t;
+  bs.fin_n = beam.fin_n;
+  bs.t = ws.t;
+  bs.alive = ws.alive;
+  bs.ticket = beam.ticket;
+  bs.out_ids = beam.out_ids;
+  bs.out_len = beam.out_len;
+  bs.scratch = beam.scratch;
+  CK(cudaMemsetAsync(beam.anc, 0, sizeof(int32_t) * 2 * (size_t)rows * cap, stream));
+  CK(launch_beam_init(bs, run.bos_id, stream));
+  ++launches;
+  StepView v = step_view(rows, cap, max_len, k);
+  v.anc = beam.anc;
+  v.anc_stride = (int64_t)rows * cap;
+  v.topk = &beam.part;
+  v.logits = dt == kF32 ? beam.logits : nullptr;
+  auto body = [&](int t) {
+    v.host_t = t;
+    run_step(v, stream);
+    int ev = prof_begin(stream);
+    CK(launch_beam_row_reduce(bs, stream));
+    CK(launch_beam_select(bs, stream));
+    prof_end(stream, ev, FNMT_K_SEARCH, 0.0, (double)rows * beam.part.tiles * 8 * (4 + beam.part.K));
+    launches += 2;
+  };
+  const int64_t nodes = profiling ? 0 : capture_step([&] { body(0); });
+  const int steps = drive_steps(cap, nodes, body);
+  CK(launch_beam_final(bs, stream));
+  ++launches;
+  return steps;
+}
+
 void Engine::lens_from_cu(int R) {
   lens_from_cu_kernel<<<(R + 255) / 256, 256, 0, stream>>>(ws.cu, ws.len, R);
   CK(cudaGetLastError());
@@ -910,14 +1075,12 @@ void Engine::ensure_meta(size_t rows, size_t cus) {
 
 // Capture one decode step (+ greedy bookkeeping) into a graph; reuse the
 // executable graph through cudaGraphExecUpdate when the topology matches.
-int64_t Engine::capture_step(const StepView& v, const GreedyState& gs) {
+int64_t Engine::capture_step(const std::function<void()>& body) {
   const int64_t l0 = launches;
   cudaGraph_t g = nullptr;
   CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeRelaxed));
   try {
-    run_step(v, stream);
-    CK(launch_greedy_update(gs, stream));
-    ++launches;
+    body();
   } catch (...) {
     cudaStreamEndCapture(stream, &g);
     if (g) cudaGraphDestroy(g);

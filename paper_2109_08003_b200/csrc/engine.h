@@ -4,6 +4,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <functional>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -79,10 +80,33 @@ struct StepView {
   const int32_t* k_start = nullptr;
   const int32_t* k_len = nullptr;
   int k_pad = 0, rows_per_seq = 1, max_k = 0;
-  const int32_t* anc = nullptr;
+  const int32_t* anc = nullptr;        // beam: 2 ancestor tables (parity of t)
+  int64_t anc_stride = 0;
   int host_t = 0;                      // host copy of the step (profiling byte counts only)
   unsigned long long* keys = nullptr;  // argmax output (greedy)
-  float* logits = nullptr;             // or full logits (protocol path)
+  float* logits = nullptr;             // or full logits (protocol path / fp32 beam)
+  const TopKPartials* topk = nullptr;  // beam: per-tile top-K partials
+};
+
+struct BeamWs {
+  std::vector<void*> owned;
+  int64_t bytes = 0;
+  int sent_cap = 0, k = 0;
+  int64_t pool_cap = 0;
+  TopKPartials part{};
+  float* rval = nullptr;
+  int32_t* ridx = nullptr;
+  double* rlogz = nullptr;
+  double* score = nullptr;
+  uint8_t* active = nullptr;
+  int32_t *anc = nullptr, *tok_hist = nullptr, *par_hist = nullptr;
+  uint8_t* finished = nullptr;
+  int32_t *n_done = nullptr, *fin_t = nullptr, *fin_n = nullptr;
+  double* done_score = nullptr;
+  int32_t *done_t = nullptr, *done_slot = nullptr;
+  uint32_t* ticket = nullptr;
+  int32_t *out_ids = nullptr, *out_len = nullptr, *scratch = nullptr;
+  float* logits = nullptr;
 };
 
 class Engine {
@@ -157,7 +181,13 @@ class Engine {
                       cudaStream_t s);
   void cross_kv_all(int n_tok, cudaStream_t s);
   void run_step(const StepView& v, cudaStream_t s);
-  int64_t capture_step(const StepView& v, const GreedyState& gs);
+  int64_t capture_step(const std::function<void()>& body);
+  int drive_steps(int cap, int64_t nodes, const std::function<void(int)>& direct);
+  StepView step_view(int rows, int cap, int max_len, int rows_per_seq);
+  int decode_greedy(int R, int cap, int max_len, const fnmt_run& run);
+  int decode_beam(int R, int cap, int max_len, const fnmt_run& run);
+  void reserve_beam(int sent_cap, int k, int64_t pool_cap);
+  BeamWs beam;
   void lens_from_cu(int R);
   void ensure_meta(size_t rows, size_t cus);
 

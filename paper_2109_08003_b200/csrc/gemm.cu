@@ -50,6 +50,7 @@ struct EpiParams {
   const float* resid;
   int ld_resid;
   unsigned long long* keys;
+  TopKPartials tk;
 };
 
 __device__ __forceinline__ float epi_value(const EpiParams& e, int m, int n, float acc) {
@@ -176,7 +177,75 @@ struct TcCfg {
 
 constexpr int kTcThreads = 192;
 
-template <int BN, int STAGES>
+// Beam epilogue for one row of one BN-wide tile: two passes over the TMEM
+// accumulator (max + running top-K, then sum of exp(x - max)); the partials
+// are merged per row by beam_row_reduce (beam.cu).
+template <int BN, int TOPK>
+__device__ __forceinline__ void topk_epilogue(const EpiParams& ep, uint32_t taddr, const float* bs,
+                                              int m, bool row_ok, int n0) {
+  float mx = -INFINITY;
+  float tv[TOPK];
+  int ti[TOPK];
+#pragma unroll
+  for (int j = 0; j < TOPK; ++j) {
+    tv[j] = -INFINITY;
+    ti[j] = -1;
+  }
+#pragma unroll 1
+  for (int c = 0; c < BN / 32; ++c) {
+    float v[32];
+    tmem_ld32(taddr + c * 32, v);
+    const int nb = n0 + c * 32;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const float x = v[i] + bs[c * 32 + i];
+      if (nb + i < ep.N) {
+        mx = fmaxf(mx, x);
+        if (x > tv[TOPK - 1]) {
+          tv[TOPK - 1] = x;
+          ti[TOPK - 1] = nb + i;
+#pragma unroll
+          for (int j = TOPK - 1; j > 0; --j) {
+            if (tv[j] > tv[j - 1]) {
+              const float fv = tv[j];
+              tv[j] = tv[j - 1];
+              tv[j - 1] = fv;
+              const int iv = ti[j];
+              ti[j] = ti[j - 1];
+              ti[j - 1] = iv;
+            }
+          }
+        }
+      }
+    }
+  }
+  double sum = 0.0;
+#pragma unroll 1
+  for (int c = 0; c < BN / 32; ++c) {
+    float v[32];
+    tmem_ld32(taddr + c * 32, v);
+    const int nb = n0 + c * 32;
+    float cs = 0.f;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const float x = v[i] + bs[c * 32 + i];
+      if (nb + i < ep.N) cs += exp2f((x - mx) * 1.4426950408889634f);
+    }
+    sum += (double)cs;
+  }
+  if (row_ok) {
+    const size_t o = (size_t)m * ep.tk.tiles + n0 / BN;
+    ep.tk.pmax[o] = mx;
+    ep.tk.psum[o] = sum;
+#pragma unroll
+    for (int j = 0; j < TOPK; ++j) {
+      ep.tk.pval[o * TOPK + j] = tv[j];
+      ep.tk.pidx[o * TOPK + j] = ti[j];
+    }
+  }
+}
+
+template <int BN, int STAGES, int TOPK>
 __global__ void __launch_bounds__(kTcThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmw,
                    int K, uint32_t idesc, EpiParams ep, int tiles_n, int tiles) {
@@ -285,20 +354,27 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       const int m = m0 + quarter * 32 + lane;
       const bool row_ok = m < ep.M;
       const uint32_t taddr = tmem + acc * BN + ((uint32_t)(quarter * 32) << 16);
-      float best_v = -INFINITY;
-      int best_i = -1;
+      if constexpr (TOPK > 0) {
+        topk_epilogue<BN, TOPK>(ep, taddr, bs, m, row_ok, n0);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tempty + acc);
+      } else {
+        float best_v = -INFINITY;
+        int best_i = -1;
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        float v[32];
-        tmem_ld32(taddr + c * 32, v);
-        const int nb = n0 + c * 32;
-        if (row_ok && nb < ep.N) epilogue_chunk(ep, m, nb, v, bs + c * 32, best_v, best_i);
+        for (int c = 0; c < BN / 32; ++c) {
+          float v[32];
+          tmem_ld32(taddr + c * 32, v);
+          const int nb = n0 + c * 32;
+          if (row_ok && nb < ep.N) epilogue_chunk(ep, m, nb, v, bs + c * 32, best_v, best_i);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tempty + acc);
+        if (ep.epi == kEpiArgmax && row_ok && best_i >= 0)
+          atomicMax(ep.keys + m, argmax_key(best_v, (uint32_t)best_i));
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(tempty + acc);
-      if (ep.epi == kEpiArgmax && row_ok && best_i >= 0)
-        atomicMax(ep.keys + m, argmax_key(best_v, (uint32_t)best_i));
       acc ^= 1;
       if (acc == 0) aph ^= 1;
     }
@@ -391,13 +467,13 @@ int num_sms() {
   return n;
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int TOPK = 0>
 cudaError_t launch_tc(const CUtensorMap& ta, const CUtensorMap& tw, const GemmArgs& g,
                       const EpiParams& ep, cudaStream_t s) {
   using Cfg = TcCfg<BN, STAGES>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<BN, STAGES>,
+    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<BN, STAGES, TOPK>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
     if (e != cudaSuccess) return e;
     attr = true;
@@ -406,8 +482,8 @@ cudaError_t launch_tc(const CUtensorMap& ta, const CUtensorMap& tw, const GemmAr
   const int tiles = tiles_n * ((g.M + kBM - 1) / kBM);
   const int grid = tiles < num_sms() ? tiles : num_sms();
   const uint32_t idesc = umma_idesc_f16(kBM, BN, g.in_dtype == kBF16);
-  gemm_tc_kernel<BN, STAGES><<<grid, kTcThreads, Cfg::kSmem, s>>>(ta, tw, g.K, idesc, ep,
-                                                                  tiles_n, tiles);
+  gemm_tc_kernel<BN, STAGES, TOPK><<<grid, kTcThreads, Cfg::kSmem, s>>>(ta, tw, g.K, idesc, ep,
+                                                                        tiles_n, tiles);
   return cudaGetLastError();
 }
 
@@ -453,7 +529,10 @@ int pick_bn(int M, int N) {
 
 cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t s) {
   if (g.M <= 0 || g.N <= 0) return cudaSuccess;
-  EpiParams ep{g.bias, g.M, g.N, g.epi, g.C, g.ldc, g.c_dtype, g.relu, g.resid, g.ld_resid, g.keys};
+  EpiParams ep{g.bias, g.M, g.N, g.epi, g.C, g.ldc, g.c_dtype, g.relu, g.resid, g.ld_resid,
+               g.keys, g.topk};
+  if (g.epi == kEpiTopK && (g.in_dtype == kF32 || (g.topk.K != 4 && g.topk.K != 8)))
+    return cudaErrorInvalidValue;   // fp32 path: store logits + launch_logits_topk_partials
   if (g.in_dtype == kF32) {
     dim3 grid((g.N + kSB - 1) / kSB, (g.M + kSB - 1) / kSB);
     gemm_simt_kernel<<<grid, 256, 0, s>>>(reinterpret_cast<const float*>(g.A), g.lda,
@@ -472,6 +551,11 @@ cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t s) {
     if (!make_tmap_16(&tw, g.W, g.in_dtype, g.N, g.K, g.ldw, kWBox, nullptr))
       return cudaErrorInvalidValue;
     pw = &tw;
+  }
+  if (g.epi == kEpiTopK) {
+    static_assert(kTopKTile == 256, "top-K partial tiles follow BN = 256");
+    return g.topk.K == 4 ? launch_tc<256, 4, 4>(*pa, *pw, g, ep, s)
+                         : launch_tc<256, 4, 8>(*pa, *pw, g, ep, s);
   }
   switch (pick_bn(g.M, g.N)) {
     case 256: return launch_tc<256, 4>(*pa, *pw, g, ep, s);

@@ -13,6 +13,19 @@ namespace fnmt {
 enum Epilogue : int {
   kEpiStore = 0,   // C[m,n] = act(acc + bias[n] (+ resid[m,n]))   in c_dtype
   kEpiArgmax = 1,  // keys[m] = max over n < valid_n of key(acc + bias[n], n)
+  kEpiTopK = 2,    // per (row, 256-column tile): max, sum exp(x - max), top-K (value, index)
+};
+
+// Per-(row, N-tile) partials of the beam epilogue; tile = n / kTopKTile.
+constexpr int kTopKTile = 256;
+constexpr int kTopKMax = 8;
+struct TopKPartials {
+  float* pmax;     // [rows][tiles]
+  double* psum;    // [rows][tiles]
+  float* pval;     // [rows][tiles][K]
+  int32_t* pidx;   // [rows][tiles][K]
+  int tiles;
+  int K;           // 4 or 8 entries kept per tile
 };
 
 struct GemmArgs {
@@ -31,6 +44,7 @@ struct GemmArgs {
   const float* resid = nullptr;  // optional fp32 residual added before store
   int ld_resid = 0;
   unsigned long long* keys = nullptr;  // argmax keys per row (must be pre-zeroed)
+  TopKPartials topk{};                 // kEpiTopK outputs
   // Pre-encoded TMA descriptors (tcgen05 path).  If null the launcher encodes
   // them on the fly (host cost ~ microseconds).
   const CUtensorMap* tmap_a = nullptr;
@@ -96,7 +110,8 @@ struct DecAttnArgs {
   int self_mode;
   int cap;                              // self: slots per row
   const int32_t* t_ptr;                 // self: device step counter
-  const int32_t* anc;                   // self beam: ancestor table [rows, cap] or null
+  const int32_t* anc;                   // self beam: ancestor tables, 2 x [rows, cap] or null
+  int64_t anc_buf_stride;               // elements between the two tables (step parity t & 1)
   const int32_t* k_start; const int32_t* k_len; int k_pad; int rows_per_seq;
   int max_k;
 };
@@ -120,6 +135,44 @@ cudaError_t launch_greedy_update(const GreedyState& g, cudaStream_t s);
 
 cudaError_t launch_keys_to_index(const unsigned long long* keys, int rows, int32_t* out,
                                  cudaStream_t s);
+
+// ---------------------------------------------------------------------------
+// beam search (search.py:105-147), batched: row = sentence * k + slot
+
+struct BeamState {
+  int nS, k, cap, rows;
+  int eos, pad;
+  TopKPartials part;            // from the vocab GEMM epilogue (or logits_topk_partials)
+  float* rval;                  // [rows][k] row top-k logits
+  int32_t* ridx;                // [rows][k]
+  double* rlogz;                // [rows] log-sum-exp of the row's logits
+  int32_t* prev;                // [rows] next decoder input
+  double* score;                // [rows]
+  uint8_t* active;              // [rows]
+  int32_t* anc;                 // 2 x [rows][cap] ancestor tables (parity t & 1)
+  int32_t* tok_hist;            // [cap][rows] token appended at step t to slot
+  int32_t* par_hist;            // [cap][rows] parent slot at step t
+  const int32_t* budget;        // [nS]
+  uint8_t* finished;            // [nS]
+  int32_t* n_done;              // [nS]
+  double* done_score;           // [nS][2k]
+  int32_t* done_t;              // [nS][2k]
+  int32_t* done_slot;           // [nS][2k]
+  int32_t* fin_t;               // [nS] step of the final active set
+  int32_t* fin_n;               // [nS] size of the final active set
+  int32_t* t;                   // device step counter
+  int32_t* alive;               // sentences still running
+  uint32_t* ticket;             // grid-completion counter (last CTA bumps t)
+  int32_t* out_ids;             // [nS][cap] final tokens
+  int32_t* out_len;             // [nS]
+  int32_t* scratch;             // [nS][2k][cap] backtracking buffer
+};
+cudaError_t launch_beam_init(const BeamState& b, int bos, cudaStream_t s);
+cudaError_t launch_logits_topk_partials(const float* logits, int rows, int n,
+                                        const TopKPartials& p, cudaStream_t s);
+cudaError_t launch_beam_row_reduce(const BeamState& b, cudaStream_t s);
+cudaError_t launch_beam_select(const BeamState& b, cudaStream_t s);
+cudaError_t launch_beam_final(const BeamState& b, cudaStream_t s);
 cudaError_t launch_argmax_rows(const float* logits, int ld, int rows, int n,
                                int32_t* out_idx, cudaStream_t s);
 cudaError_t launch_gather_rows(const void* src, void* dst, const int32_t* idx, int rows,

@@ -79,9 +79,10 @@ class Engine:
         return b, off
 
     def translate(self, ids: np.ndarray, offsets: np.ndarray, sbatch=3072, wbatch=64000,
-                  ratio=1.5, offset=5, out_ids=None, out_len=None, out_off=None):
+                  ratio=1.5, offset=5, out_ids=None, out_len=None, out_off=None, beam=1):
         """Host buffers.  ids int32 (flat), offsets int64 [n+1].  Returns
-        (out_ids flat int32 laid out at out_off, out_len int32 [n], out_off, stats)."""
+        (out_ids flat int32 laid out at out_off, out_len int32 [n], out_off, stats).
+        beam > 1 runs the batched device beam search (search.py:105-147)."""
         ids = np.ascontiguousarray(ids, dtype=np.int32) if isinstance(ids, np.ndarray) else ids
         offsets = np.ascontiguousarray(offsets, dtype=np.int64) if isinstance(
             offsets, np.ndarray) else offsets
@@ -97,7 +98,7 @@ class Engine:
         if out_len is None:
             out_len = np.empty(max(n, 1), dtype=np.int32)
         st = _capi.fnmt_stats()
-        r = run_struct(sbatch, wbatch, ratio, offset)
+        r = run_struct(sbatch, wbatch, ratio, offset, beam)
         check(lib.fnmt_engine_translate(self.handle.h, ptr(ids), ptr(offsets), n, C.byref(r),
                                         ptr(out_ids), ptr(out_off), ptr(out_len), C.byref(st)),
               "translate")
@@ -105,10 +106,11 @@ class Engine:
 
     def translate_device(self, d_ids: torch.Tensor, d_offsets: torch.Tensor, lengths: np.ndarray,
                          d_out_ids: torch.Tensor, out_off: np.ndarray, d_out_off: torch.Tensor,
-                         d_out_len: torch.Tensor, sbatch=3072, wbatch=64000, ratio=1.5, offset=5):
+                         d_out_len: torch.Tensor, sbatch=3072, wbatch=64000, ratio=1.5, offset=5,
+                         beam=1):
         lengths = np.ascontiguousarray(lengths, dtype=np.int32)
         st = _capi.fnmt_stats()
-        r = run_struct(sbatch, wbatch, ratio, offset)
+        r = run_struct(sbatch, wbatch, ratio, offset, beam)
         check(lib.fnmt_engine_translate_device(
             self.handle.h, ptr(d_ids), ptr(d_offsets), lengths.ctypes.data, len(lengths),
             C.byref(r), ptr(d_out_ids), out_off.ctypes.data, ptr(d_out_off), ptr(d_out_len),
@@ -132,7 +134,9 @@ class Engine:
 
 
 def translate_ids(handle, rows, search=None, sbatch=3072, wbatch=64000) -> list[list[int]]:
-    """Greedy-translate a list of id sequences through the native corpus path."""
+    """Translate a list of id sequences through the native corpus path (greedy,
+    or batched beam when search.beam_size > 1)."""
+    beam = getattr(search, "beam_size", 1)
     ratio = getattr(search, "max_len_ratio", 1.5)
     offset = getattr(search, "max_len_offset", 5)
     bos = getattr(search, "bos_id", BOS_ID)
@@ -155,7 +159,7 @@ def translate_ids(handle, rows, search=None, sbatch=3072, wbatch=64000) -> list[
     out_ids = np.empty(max(int(budgets.sum()), 1), dtype=np.int32)
     out_len = np.empty(n, dtype=np.int32)
     st = _capi.fnmt_stats()
-    r = run_struct(sbatch, min(wbatch, int(lengths.max(initial=1)) * n), ratio, offset, 1, bos,
+    r = run_struct(sbatch, min(wbatch, int(lengths.max(initial=1)) * n), ratio, offset, beam, bos,
                    eos, pad)
     check(lib.fnmt_engine_translate(handle.h, ids.ctypes.data, offsets.ctypes.data, n,
                                     C.byref(r), out_ids.ctypes.data, out_off.ctypes.data,

@@ -252,8 +252,14 @@ class GpuTranslationModel:
         return out.cpu().numpy()
 
     def beam_batch(self, enc: GpuEncoderOutput, cfg) -> list[list[int]]:
-        """Beam search per sentence over the device decoder (search.py:105-147)."""
-        from .search import _beam_sentence
+        """Beam search (search.py:105-147).  Batched on the device: fused
+        vocab top-K epilogue, per-sentence selection kernel, ancestor-table
+        KV reuse.  Rows whose source is entirely masked keep the reference's
+        all-masked attention semantics through the protocol loop."""
+        from .search import _beam_sentence, _device_rows
+        rows = _device_rows(self, enc)
+        if rows is not None:
+            return self.translate_batch(rows, search=cfg)
         lens = enc.pad_mask.sum(axis=1)
         return [_beam_sentence(self, self.init_cache(enc.row(r)), int(lens[r]), cfg)
                 for r in range(enc.pad_mask.shape[0])]

@@ -1,0 +1,100 @@
+"""Native batched beam search (fused top-K vocab epilogue + per-sentence
+selection kernel + ancestor-table KV reuse) against the reference semantics
+(search.py:105-147): reference fixtures on student models, and the oracle on
+tiny models whose EOS bias is raised so that hypotheses finish at different
+steps (EOS consumes beam slots, stop at k finished, final pick over the
+finished pool)."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from oracle import nmt_oracle as O  # noqa: E402
+from paper_2109_08003_b200 import store as S  # noqa: E402
+from paper_2109_08003_b200.engine import Engine  # noqa: E402
+from paper_2109_08003_b200.model import GpuTranslationModel  # noqa: E402
+from paper_2109_08003_b200.search import SearchConfig, beam_translate, greedy_translate  # noqa: E402
+
+
+def split(ids, lens):
+    out, o = [], 0
+    for n in lens:
+        out.append([int(x) for x in ids[o:o + n]])
+        o += int(n)
+    return out
+
+
+def run_engine(eng, rows, k, sbatch=3072, wbatch=64000):
+    lengths = np.array([len(r) for r in rows])
+    offsets = np.concatenate([[0], np.cumsum(lengths)]).astype(np.int64)
+    out, olen, off, _ = eng.translate(np.concatenate(rows).astype(np.int32), offsets,
+                                      sbatch=sbatch, wbatch=wbatch, beam=k)
+    return [out[o:o + n].tolist() for o, n in zip(off, olen)]
+
+
+@pytest.mark.parametrize("tag", ["student_6_1_1", "student_6_1_8"])
+@pytest.mark.parametrize("dtype", ["f32", "f16"])
+def test_student_beam_vs_reference(golden, tag, dtype):
+    g = golden("beam_students")
+    heads = 1 if tag.endswith("1_1") else 8
+    cfg = S.ModelConfig(6, 1, 512, heads, heads, 2048, 2048, 32772, 1024)
+    eng = Engine(cfg, S.random_model(cfg, 0), dtype=dtype)
+    rows = split(g["src_ids"], g["src_lens"])
+    for k in (2, 4):
+        want = split(g[f"{tag}_beam{k}_ids"], g[f"{tag}_beam{k}_lens"])
+        got = run_engine(eng, rows, k)
+        same = sum(a == b for a, b in zip(got, want))
+        if dtype == "f32":
+            assert got == want, (k, same)
+        else:
+            assert same >= len(rows) - 1, (k, same)
+
+
+def eos_biased(cfg, seed, bias):
+    w = S.random_model(cfg, seed)
+    w.out_proj.bias[3] += np.float32(bias)      # raise EOS (id 3)
+    return w
+
+
+@pytest.mark.parametrize("k", [2, 3, 4, 8])
+@pytest.mark.parametrize("bias", [0.0, 1.0, 2.0, 3.0])
+def test_beam_with_eos_matches_oracle(k, bias):
+    cfg = S.ModelConfig(2, 1, 32, 2, 2, 64, 32, 40, 64)
+    w = eos_biased(cfg, 7, bias)
+    a = O.arch_of(cfg)
+    p = O.make_params(a, 7)
+    p["out_bias"] = p["out_bias"].copy()
+    p["out_bias"][3] += np.float32(bias)
+    rng = np.random.default_rng(int(bias * 10) + k)
+    rows = [rng.integers(4, cfg.vocab_size, size=int(rng.integers(1, 12))) for _ in range(24)]
+    tok, valid = O.pad_rows(rows)
+    want = O.beam(a, p, tok, valid, k)
+    eng = Engine(cfg, w, dtype="f32")
+    got = run_engine(eng, rows, k)
+    assert got == want
+    # batch composition must not matter
+    got_small = run_engine(eng, rows, k, sbatch=5, wbatch=40)
+    assert got_small == want
+    eng16 = Engine(cfg, w, dtype="f16")
+    got16 = run_engine(eng16, rows, k)
+    assert sum(x == y for x, y in zip(got16, want)) >= len(rows) - 2
+
+
+def test_beam1_equals_greedy_native(golden):
+    """Reference acceptance 'greedy-beam1-equivalence' (tests/test_acceptance.py:246-269)."""
+    for seed in range(6):
+        cfg = S.ModelConfig(2, 1, 32, 2, 1, 64, 32, 48, 64, norm_variant="l1" if seed % 2 else "l2")
+        w = eos_biased(cfg, seed, 1.5)
+        m = GpuTranslationModel(cfg, w, dtype="f32")
+        rng = np.random.default_rng(seed)
+        rows = [rng.integers(4, 48, size=int(rng.integers(2, 9))) for _ in range(7)]
+        tok, valid = O.pad_rows(rows)
+        enc = m.encode(tok, valid)
+        g1 = greedy_translate(m, enc, SearchConfig(2, 3, 0))
+        b1 = beam_translate(m, enc, SearchConfig(2, 3, 0, beam_size=1))
+        assert g1 == b1, seed

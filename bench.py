@@ -40,6 +40,18 @@ CFG = dict(n_enc_layers=6, n_dec_layers=1, d_model=512, n_heads_enc=1, n_heads_d
            ffn_dim_enc=2048, ffn_dim_dec=2048, vocab_size=32772, max_positions=1024)
 SBATCH, WBATCH = 3072, 64000
 
+# BASELINE.json configs 2-5 (SURVEY §8 model shapes)
+MODELS = {
+    "6-1-1": ("Student-6-1-1 (6-1, d512, 1/1 heads, ffn 2048/2048, V 32772)", CFG),
+    "6-1-8": ("Student-6-1-8 (6-1, d512, 8/8 heads, ffn 2048/2048, V 32772)",
+              dict(CFG, n_heads_enc=8, n_heads_dec=8)),
+    "6-6-8": ("Student-6-6-8 (6-6, d512, 8/8 heads, ffn 2048/2048, V 32772, unshared)",
+              dict(CFG, n_dec_layers=6, n_heads_enc=8, n_heads_dec=8, shared_embeddings=False)),
+    "deep-12-768": ("Deep-12-768 (12-6, d768, 8/8 heads, ffn 3072/3072, V 32772)",
+                    dict(CFG, n_enc_layers=12, n_dec_layers=6, d_model=768, n_heads_enc=8,
+                         n_heads_dec=8, ffn_dim_enc=3072, ffn_dim_dec=3072)),
+}
+
 
 def parse():
     ap = argparse.ArgumentParser()
@@ -54,6 +66,8 @@ def parse():
     ap.add_argument("--profile-sentences", type=int, default=16384)
     ap.add_argument("--wbatch", type=int, default=64000, help="token cap (paper GPU setting 64000)")
     ap.add_argument("--sbatch", type=int, default=3072, help="sentence cap (paper GPU setting 3072)")
+    ap.add_argument("--model", choices=sorted(MODELS), default="6-1-1")
+    ap.add_argument("--beam", type=int, default=1)
     return ap.parse_args()
 
 
@@ -262,7 +276,9 @@ def main():
     from paper_2109_08003_b200.engine import Engine, budgets_of
     from paper_2109_08003_b200.synthetic import newstest_corpus
 
-    cfg = S.ModelConfig(**CFG)
+    model_desc, model_cfg = MODELS[args.model]
+    cfg = S.ModelConfig(**model_cfg)
+    BEAM = args.beam
     ids, offsets, lengths = newstest_corpus(CORPUS, cfg.vocab_size)
     C = args.chunk_sentences
     n_chunks = max(1, CORPUS // C)
@@ -294,7 +310,8 @@ def main():
         lo, hi, L, b, off = chunk_meta[c]
         flush.zero_()
         return eng.translate_device(d_ids, d_offsets[lo:hi + 1], L, d_out_ids, off,
-                                    d_out_off[c], d_out_len[slot], sbatch=SBATCH, wbatch=WBATCH)
+                                    d_out_off[c], d_out_len[slot], sbatch=SBATCH, wbatch=WBATCH,
+                                    beam=BEAM)
 
     for i in range(W):
         device_step(chunk_of(i), 0)
@@ -338,7 +355,7 @@ def main():
         n_ids = int(offsets[hi] - offsets[lo])
         eng.translate(pin_ids[int(offsets[lo]):int(offsets[hi])].numpy(), offsets[lo:hi + 1],
                       sbatch=SBATCH, wbatch=WBATCH, out_ids=pin_out.numpy(),
-                      out_len=pin_len.numpy(), out_off=off)
+                      out_len=pin_len.numpy(), out_off=off, beam=BEAM)
         return n_ids * 4 + (hi - lo + 1) * 8 + (hi - lo) * 8, int(b.sum()) * 4 + (hi - lo) * 4
 
     host_step(chunk_of(0))
@@ -377,7 +394,7 @@ def main():
         eng.profile(True)
         eng.translate_device(d_ids, d_offsets[lo:hi + 1], L, d_out_ids, off,
                              torch.from_numpy(off).to(device), d_out_len[0], sbatch=SBATCH,
-                             wbatch=WBATCH)
+                             wbatch=WBATCH, beam=BEAM)
         prof = eng.profile_read()
         eng.profile(False)
 
@@ -433,10 +450,12 @@ def main():
         "steps": K, "warmup": W, "ms_per_step": round(1e3 * t_max / max(K, 1), 2),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": args.dtype, "data": "synthetic",
-        "config": {"workload": "Student-6-1-1 fp16 greedy, 1M (2^20) synthetic newstest-shaped "
-                               "sentences, dynamic batching sbatch/wbatch 3072/64000",
-                   "model": "Student-6-1-1 (6-1, d512, 1/1 heads, ffn 2048/2048, V 32772, "
-                            "random-init seed 0)",
+        "config": {"workload": f"{model_desc.split(' (')[0]} {args.dtype} "
+                               f"{'greedy' if BEAM == 1 else f'beam={BEAM}'}, 1M (2^20) synthetic "
+                               f"newstest-shaped sentences, dynamic batching sbatch/wbatch "
+                               f"{SBATCH}/{WBATCH}",
+                   "model": f"{model_desc[:-1]}, random-init seed 0)",
+                   "beam": BEAM,
                    "corpus_sentences": CORPUS, "chunk_sentences": C,
                    "sentences_per_step_all_ranks": C * world,
                    "parallelism": f"sentence-sharded dp{world} (no collective)",

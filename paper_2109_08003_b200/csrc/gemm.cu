@@ -175,14 +175,17 @@ struct TcCfg {
   static constexpr int kSmem = 1024 + STAGES * kStage + 2 * BN * 4 + 256;
 };
 
-constexpr int kTcThreads = 192;
+constexpr int kEpiWarps = 8;                       // 2 per TMEM lane quarter
+constexpr int kTcThreads = 64 + kEpiWarps * 32;    // producer + MMA warps, epilogue
 
-// Beam epilogue for one row of one BN-wide tile: two passes over the TMEM
-// accumulator (max + running top-K, then sum of exp(x - max)); the partials
-// are merged per row by beam_row_reduce (beam.cu).
+// Beam epilogue for one row of one 128-column half tile (kTopKTile): two
+// passes over the TMEM accumulator (max + running top-K, then sum of
+// exp(x - max)); the partials are merged per row by beam_row_reduce (beam.cu).
+// `taddr`/`bs`/`n0` point at the first column of this warp's half.
 template <int BN, int TOPK>
 __device__ __forceinline__ void topk_epilogue(const EpiParams& ep, uint32_t taddr, const float* bs,
                                               int m, bool row_ok, int n0) {
+  static_assert(BN / 2 == kTopKTile, "half tile == top-K partial tile");
   float mx = -INFINITY;
   float tv[TOPK];
   int ti[TOPK];
@@ -192,7 +195,7 @@ __device__ __forceinline__ void topk_epilogue(const EpiParams& ep, uint32_t tadd
     ti[j] = -1;
   }
 #pragma unroll 1
-  for (int c = 0; c < BN / 32; ++c) {
+  for (int c = 0; c < BN / 64; ++c) {
     float v[32];
     tmem_ld32(taddr + c * 32, v);
     const int nb = n0 + c * 32;
@@ -221,7 +224,7 @@ __device__ __forceinline__ void topk_epilogue(const EpiParams& ep, uint32_t tadd
   }
   double sum = 0.0;
 #pragma unroll 1
-  for (int c = 0; c < BN / 32; ++c) {
+  for (int c = 0; c < BN / 64; ++c) {
     float v[32];
     tmem_ld32(taddr + c * 32, v);
     const int nb = n0 + c * 32;
@@ -233,8 +236,8 @@ __device__ __forceinline__ void topk_epilogue(const EpiParams& ep, uint32_t tadd
     }
     sum += (double)cs;
   }
-  if (row_ok) {
-    const size_t o = (size_t)m * ep.tk.tiles + n0 / BN;
+  if (row_ok && n0 < ep.N) {   // a half tile entirely past N has no partial slot
+    const size_t o = (size_t)m * ep.tk.tiles + n0 / kTopKTile;
     ep.tk.pmax[o] = mx;
     ep.tk.psum[o] = sum;
 #pragma unroll
@@ -275,7 +278,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(tfull + b, 1);
-      mbar_init(tempty + b, 4);
+      mbar_init(tempty + b, kEpiWarps);
     }
     fence_mbar_init();
   }
@@ -337,8 +340,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       }
     }
   } else {
-    // epilogue warps 2..5: TMEM lane quarter = warp % 4
+    // epilogue warps 2..9: TMEM lane quarter = warp % 4 (hardware rule), and
+    // the two warps of a quarter split the tile's columns in halves.
     const int quarter = warp & 3;
+    const int half = (warp - 2) >> 2;
     int acc = 0;
     uint32_t aph = 0;
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
@@ -346,16 +351,17 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       const int n0 = (tile % tiles_n) * BN;
       // stage this tile's bias while the MMAs run (double-buffered by acc)
       float* bs = bias_s + acc * BN;
-      for (int i = threadIdx.x - 64; i < BN; i += 128)
+      for (int i = threadIdx.x - 64; i < BN; i += kEpiWarps * 32)
         bs[i] = (ep.bias && n0 + i < ep.N) ? ep.bias[n0 + i] : 0.f;
-      named_bar_sync(1, 128);
+      named_bar_sync(1, kEpiWarps * 32);
       mbar_wait(tfull + acc, aph);
       tc_fence_after();
       const int m = m0 + quarter * 32 + lane;
       const bool row_ok = m < ep.M;
-      const uint32_t taddr = tmem + acc * BN + ((uint32_t)(quarter * 32) << 16);
+      const int col0 = half * (BN / 2);
+      const uint32_t taddr = tmem + acc * BN + col0 + ((uint32_t)(quarter * 32) << 16);
       if constexpr (TOPK > 0) {
-        topk_epilogue<BN, TOPK>(ep, taddr, bs, m, row_ok, n0);
+        topk_epilogue<BN, TOPK>(ep, taddr, bs + col0, m, row_ok, n0 + col0);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(tempty + acc);
@@ -363,11 +369,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         float best_v = -INFINITY;
         int best_i = -1;
 #pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
+        for (int c = 0; c < BN / 64; ++c) {
           float v[32];
           tmem_ld32(taddr + c * 32, v);
-          const int nb = n0 + c * 32;
-          if (row_ok && nb < ep.N) epilogue_chunk(ep, m, nb, v, bs + c * 32, best_v, best_i);
+          const int nb = n0 + col0 + c * 32;
+          if (row_ok && nb < ep.N)
+            epilogue_chunk(ep, m, nb, v, bs + col0 + c * 32, best_v, best_i);
         }
         tc_fence_before();
         __syncwarp();
@@ -553,7 +560,7 @@ cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t s) {
     pw = &tw;
   }
   if (g.epi == kEpiTopK) {
-    static_assert(kTopKTile == 256, "top-K partial tiles follow BN = 256");
+    static_assert(kTopKTile == 128, "top-K partial tiles are half of BN = 256");
     return g.topk.K == 4 ? launch_tc<256, 4, 4>(*pa, *pw, g, ep, s)
                          : launch_tc<256, 4, 8>(*pa, *pw, g, ep, s);
   }

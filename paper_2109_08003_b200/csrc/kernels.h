@@ -17,7 +17,7 @@ enum Epilogue : int {
 };
 
 // Per-(row, N-tile) partials of the beam epilogue; tile = n / kTopKTile.
-constexpr int kTopKTile = 256;
+constexpr int kTopKTile = 128;
 constexpr int kTopKMax = 8;
 struct TopKPartials {
   float* pmax;     // [rows][tiles]

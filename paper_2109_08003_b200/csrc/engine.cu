@@ -472,6 +472,20 @@ void Engine::reserve(int tok_cap, int row_cap, int64_t pool_cap) {
               make_tmap_16(&ws.tm_datt, ws.datt, dt, row_cap, d, d, 128, &err) &&
               make_tmap_16(&ws.tm_dh, ws.dh, dt, row_cap, fd, fd, 128, &err);
     if (!ok) throw EngineError(FNMT_E_CUDA, "workspace TMA descriptor: " + err);
+    // decode-attention K/V maps (box = KC keys x min(dk, 256) dims)
+    // Off by default: measured slower than attn_decode_kernel (r01: 79 ms vs 44 ms per 16k
+    // sentences) because the 96 KB stage ring limits residency to 2 CTAs/SM.
+    const int dkd = d / arch.n_heads_dec;
+    ws.kv_tma = getenv("FNMT_DECODE_TMA") != nullptr && dkd % 8 == 0 &&
+                (dkd <= 256 || dkd % 256 == 0);
+    ws.tm_sk.resize(arch.n_dec_layers);
+    ws.tm_sv.resize(arch.n_dec_layers);
+    ws.tm_ckv.resize(arch.n_dec_layers);
+    for (int l = 0; l < arch.n_dec_layers && ws.kv_tma; ++l) {
+      ws.kv_tma = make_tmap_kv(&ws.tm_sk[l], ws.kc[l], dt, pool_cap, d, d, dkd, &err) &&
+                  make_tmap_kv(&ws.tm_sv[l], ws.vc[l], dt, pool_cap, d, d, dkd, &err) &&
+                  make_tmap_kv(&ws.tm_ckv[l], ws.ckv[l], dt, tok_cap, 2 * d, 2 * d, dkd, &err);
+    }
   }
   ws.bytes = device_bytes - before;
 }
@@ -640,7 +654,10 @@ void Engine::run_step(const StepView& v, cudaStream_t s) {
     a.max_k = v.cap;
     {
       const int ev = prof_begin(s);
-      CK(launch_attention_decode(a, s));
+      if (v.ws_caches && ws.kv_tma && !v.anc && tc)
+        CK(launch_attention_decode_tma(a, ws.tm_sk[l], ws.tm_sv[l], 0, 0, s));
+      else
+        CK(launch_attention_decode(a, s));
       prof_end(s, ev, FNMT_K_ATTN_DEC, 0.0, (double)R * (v.host_t + 1) * 2 * d * es);
     }
     ++launches;
@@ -667,7 +684,10 @@ void Engine::run_step(const StepView& v, cudaStream_t s) {
     c.max_k = v.max_k;
     {
       const int ev = prof_begin(s);
-      CK(launch_attention_decode(c, s));
+      if (v.ws_caches && ws.kv_tma && tc)
+        CK(launch_attention_decode_tma(c, ws.tm_ckv[l], ws.tm_ckv[l], 0, d, s));
+      else
+        CK(launch_attention_decode(c, s));
       prof_end(s, ev, FNMT_K_ATTN_DEC, 0.0, (double)R * v.max_k * 2 * d * es);
     }
     ++launches;
@@ -907,6 +927,7 @@ StepView Engine::step_view(int rows, int cap, int max_len, int rows_per_seq) {
   v.k_pad = 0;
   v.rows_per_seq = rows_per_seq;
   v.max_k = max_len;
+  v.ws_caches = true;
   return v;
 }
 

@@ -68,6 +68,9 @@ struct Workspace {
   int32_t *t = nullptr, *alive = nullptr;
   uint8_t* finished = nullptr;
   CUtensorMap tm_xa, tm_att, tm_h, tm_dxa, tm_datt, tm_dh;
+  // decode attention K/V tiles (16-bit caches): self K, self V, cross K|V per layer
+  std::vector<CUtensorMap> tm_sk, tm_sv, tm_ckv;
+  bool kv_tma = false;
 };
 
 struct StepView {
@@ -83,6 +86,7 @@ struct StepView {
   const int32_t* anc = nullptr;        // beam: 2 ancestor tables (parity of t)
   int64_t anc_stride = 0;
   int host_t = 0;                      // host copy of the step (profiling byte counts only)
+  bool ws_caches = false;              // kc/vc/ckv are the workspace buffers (TMA maps valid)
   unsigned long long* keys = nullptr;  // argmax output (greedy)
   float* logits = nullptr;             // or full logits (protocol path / fp32 beam)
   const TopKPartials* topk = nullptr;  // beam: per-tile top-K partials

@@ -524,6 +524,34 @@ bool make_tmap_16(CUtensorMap* out, const void* base, int dtype, int64_t rows, i
   return true;
 }
 
+bool make_tmap_kv(CUtensorMap* out, const void* base, int dtype, int64_t rows, int64_t cols,
+                  int64_t ld, int dk, std::string* err) {
+  auto fn = encode_fn();
+  if (!fn) {
+    if (err) *err = "cuTensorMapEncodeTiled unavailable";
+    return false;
+  }
+  const int bc = dk < 256 ? dk : 256;
+  if ((reinterpret_cast<uintptr_t>(base) & 15) || ((ld * 2) & 15) || ((bc * 2) & 15) ||
+      (dk % bc)) {
+    if (err) *err = "KV tensor map: misaligned base / leading dim / head size";
+    return false;
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
+  cuuint32_t box[2] = {(cuuint32_t)bc, (cuuint32_t)decode_tma_keys_per_chunk(dk, dtype)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(out, dtype == kBF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
+                  2, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    if (err) *err = "cuTensorMapEncodeTiled (KV) failed with CUresult " + std::to_string((int)r);
+    return false;
+  }
+  return true;
+}
+
 // N tile: the largest of 256/128/64 that still gives about one wave of tiles.
 int pick_bn(int M, int N) {
   const int mt = (M + kBM - 1) / kBM;

@@ -117,6 +117,17 @@ struct DecAttnArgs {
 };
 cudaError_t launch_attention_decode(const DecAttnArgs& a, cudaStream_t s);
 
+// TMA-fed variant (16-bit caches, no ancestor table): K/V tiles of KC keys
+// x min(dk, 256) columns are streamed through a 3-stage smem ring by 2-D
+// tensor maps `tk` / `tv` (rows = cache rows, cols = model dims); the key
+// columns of head h start at k_col0 + h*dk, values at v_col0 + h*dk.
+int decode_tma_keys_per_chunk(int dk, int dtype);
+bool make_tmap_kv(CUtensorMap* out, const void* base, int dtype, int64_t rows, int64_t cols,
+                  int64_t ld, int dk, std::string* err);
+cudaError_t launch_attention_decode_tma(const DecAttnArgs& a, const CUtensorMap& tk,
+                                        const CUtensorMap& tv, int k_col0, int v_col0,
+                                        cudaStream_t s);
+
 // ---------------------------------------------------------------------------
 // search bookkeeping (search.py:58-86)
 

@@ -218,14 +218,16 @@ __device__ __forceinline__ DecCtx decode_setup(const DecAttnArgs& a, int r, int 
   if (a.self_mode) {
     c.t = *a.t_ptr;
     c.nk = c.t + 1;
-    T* kw = reinterpret_cast<T*>(a.k_w);
-    T* vw = reinterpret_cast<T*>(a.v_w);
-    const T* nkp = reinterpret_cast<const T*>(a.new_k) + (size_t)r * a.ld_new + h * a.dk;
-    const T* nvp = reinterpret_cast<const T*>(a.new_v) + (size_t)r * a.ld_new + h * a.dk;
-    const size_t slot = ((size_t)r * a.cap + c.t) * a.ldkv + h * a.dk;
-    for (int e = threadIdx.x; e < a.dk; e += blockDim.x) {
-      kw[slot + e] = nkp[e];
-      vw[slot + e] = nvp[e];
+    if (a.new_k) {   // append this step's k/v (unless the QKV GEMM epilogue already did)
+      T* kw = reinterpret_cast<T*>(a.k_w);
+      T* vw = reinterpret_cast<T*>(a.v_w);
+      const T* nkp = reinterpret_cast<const T*>(a.new_k) + (size_t)r * a.ld_new + h * a.dk;
+      const T* nvp = reinterpret_cast<const T*>(a.new_v) + (size_t)r * a.ld_new + h * a.dk;
+      const size_t slot = ((size_t)r * a.cap + c.t) * a.ldkv + h * a.dk;
+      for (int e = threadIdx.x; e < a.dk; e += blockDim.x) {
+        kw[slot + e] = nkp[e];
+        vw[slot + e] = nvp[e];
+      }
     }
   } else {
     const int seq = r / a.rows_per_seq;
@@ -362,6 +364,151 @@ __global__ void __launch_bounds__(NT) attn_decode_kernel(DecAttnArgs a, float qs
   for (int e = tid; e < dk; e += NT) {
     float sum = red[e];
     for (int gg = 1; gg < groups; ++gg) sum += red[gg * dk + e];
+    out[e] = from_f32<T>(sum);
+  }
+}
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)),
+               "l"(gmem_src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+}
+template <typename T>
+__device__ __forceinline__ void smem16(const T* p, float (&f)[Vec16<T>::N]) {
+  load16(p, f);
+}
+
+// Same contract as attn_decode_kernel, latency-hiding version: every lane
+// stages its 16-byte chunks of U keys with cp.async into a private smem slot
+// (no register cost, U x more bytes in flight), waits once, then computes.
+// Both passes (q.K scores, then weights.V) walk keys warp-cooperatively:
+// G lanes per key, 32/G keys per warp round.
+template <typename T, int G, int CH, int NT>
+__global__ void __launch_bounds__(NT) attn_decode_async_kernel(DecAttnArgs a, float qscale) {
+  constexpr int VEC = Vec16<T>::N;
+  constexpr int U = 8;                       // warp rounds staged per batch
+  constexpr int KPW = 32 / G;
+  constexpr int NW = NT / 32;
+  extern __shared__ __align__(16) uint8_t smem_a[];
+  const int dk = a.dk;
+  // per-lane staging: [warp][U][lane][CH] x 16 B
+  uint8_t* stage = smem_a;
+  float* qs = reinterpret_cast<float*>(smem_a + (size_t)NW * U * 32 * CH * 16);
+  float* S = qs + dk;
+  float* red = S + a.max_k + 4;              // [NW][dk]
+  const int r = blockIdx.x, h = blockIdx.y;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const DecCtx c = decode_setup<T>(a, r, h);
+  const T* q = reinterpret_cast<const T*>(a.q) + (size_t)r * a.ldq + h * dk;
+  for (int e = tid; e < dk; e += NT) qs[e] = to_f32(q[e]) * qscale;
+  __syncthreads();
+
+  const int g = lane / G, li = lane % G;
+  uint8_t* my = stage + (((size_t)warp * U) * 32 + lane) * CH * 16;   // + u * 32 * CH * 16
+  const T* kb = reinterpret_cast<const T*>(a.k) + h * dk;
+  const T* vb = reinterpret_cast<const T*>(a.v) + h * dk;
+  const int round = NW * KPW;                // keys per CTA round
+  // ---- pass 1: scores ----------------------------------------------------------
+  for (int j0 = warp * KPW; j0 < c.nk; j0 += round * U) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = j0 + u * round + g;
+      if (j < c.nk) {
+        const T* kr = kb + decode_key_row(a, c, r, j) * a.ldkv;
+#pragma unroll
+        for (int ch = 0; ch < CH; ++ch) {
+          const int e0 = (li + ch * G) * VEC;
+          if (e0 < dk) cp_async16(my + ((size_t)u * 32 * CH + ch) * 16, kr + e0);
+        }
+      }
+    }
+    cp_async_wait_all();
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = j0 + u * round + g;
+      float s = 0.f;
+      if (j < c.nk) {
+#pragma unroll
+        for (int ch = 0; ch < CH; ++ch) {
+          const int e0 = (li + ch * G) * VEC;
+          if (e0 < dk) {
+            float f[VEC];
+            smem16(reinterpret_cast<const T*>(my + ((size_t)u * 32 * CH + ch) * 16), f);
+#pragma unroll
+            for (int i = 0; i < VEC; ++i) s = fmaf(qs[e0 + i], f[i], s);
+          }
+        }
+      }
+#pragma unroll
+      for (int o = G / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (li == 0 && j < c.nk) S[j] = c.all_masked ? s + kMaskValue : s;
+    }
+  }
+  __syncthreads();
+  if (warp == 0) softmax_inplace(S, c.nk);
+  __syncthreads();
+  // ---- pass 2: weights . V (lane owns chunks li + ch*G of its key group) ----------
+  float acc[CH][VEC];
+#pragma unroll
+  for (int ch = 0; ch < CH; ++ch)
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) acc[ch][i] = 0.f;
+  for (int j0 = warp * KPW; j0 < c.nk; j0 += round * U) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = j0 + u * round + g;
+      if (j < c.nk) {
+        const T* vr = vb + decode_key_row(a, c, r, j) * a.ldkv;
+#pragma unroll
+        for (int ch = 0; ch < CH; ++ch) {
+          const int e0 = (li + ch * G) * VEC;
+          if (e0 < dk) cp_async16(my + ((size_t)u * 32 * CH + ch) * 16, vr + e0);
+        }
+      }
+    }
+    cp_async_wait_all();
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = j0 + u * round + g;
+      if (j < c.nk) {
+        const float w = S[j];
+#pragma unroll
+        for (int ch = 0; ch < CH; ++ch) {
+          const int e0 = (li + ch * G) * VEC;
+          if (e0 < dk) {
+            float f[VEC];
+            smem16(reinterpret_cast<const T*>(my + ((size_t)u * 32 * CH + ch) * 16), f);
+#pragma unroll
+            for (int i = 0; i < VEC; ++i) acc[ch][i] = fmaf(w, f[i], acc[ch][i]);
+          }
+        }
+      }
+    }
+  }
+  // reduce over the KPW key groups of the warp (fixed xor order), then over warps
+#pragma unroll
+  for (int ch = 0; ch < CH; ++ch)
+#pragma unroll
+    for (int i = 0; i < VEC; ++i)
+#pragma unroll
+      for (int o = G; o < 32; o <<= 1) acc[ch][i] += __shfl_xor_sync(0xffffffffu, acc[ch][i], o);
+  if (g == 0) {
+#pragma unroll
+    for (int ch = 0; ch < CH; ++ch) {
+      const int e0 = (li + ch * G) * VEC;
+      if (e0 < dk)
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) red[warp * dk + e0 + i] = acc[ch][i];
+    }
+  }
+  __syncthreads();
+  T* out = reinterpret_cast<T*>(a.out) + (size_t)r * a.ldo + h * dk;
+  for (int e = tid; e < dk; e += NT) {
+    float sum = red[e];
+    for (int w = 1; w < NW; ++w) sum += red[w * dk + e];
     out[e] = from_f32<T>(sum);
   }
 }
@@ -569,9 +716,30 @@ cudaError_t launch_dec_nt(const DecAttnArgs& a, float qscale, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+template <typename T, int G, int CH, int NT>
+cudaError_t launch_dec_async(const DecAttnArgs& a, float qscale, cudaStream_t s) {
+  constexpr int NW = NT / 32;
+  const size_t smem = (size_t)NW * 8 * 32 * CH * 16 +
+                      sizeof(float) * ((size_t)a.dk + a.max_k + 4 + (size_t)NW * a.dk);
+  if (smem > 227 * 1024) return launch_dec_nt<T, G, CH, NT>(a, qscale, s);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(attn_decode_async_kernel<T, G, CH, NT>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  attn_decode_async_kernel<T, G, CH, NT><<<dim3(a.rows, a.heads), NT, smem, s>>>(a, qscale);
+  return cudaGetLastError();
+}
+
 template <typename T, int G, int CH>
 cudaError_t launch_dec(const DecAttnArgs& a, float qscale, cudaStream_t s) {
   // few (row, head) blocks -> wide blocks so the SMs still have enough warps in flight
+  // cp.async staging measured faster for 8 heads (dk=64) only (r01: 6-1-8 3.92M vs 3.67M
+  // words/s; 6-1-1 3.92M vs 4.32M)
+  if (G < 32) {
+    if ((int64_t)a.rows * a.heads < 1200) return launch_dec_async<T, G, CH, 256>(a, qscale, s);
+    return launch_dec_async<T, G, CH, 128>(a, qscale, s);
+  }
   if ((int64_t)a.rows * a.heads < 1200) return launch_dec_nt<T, G, CH, 512>(a, qscale, s);
   return launch_dec_nt<T, G, CH, 128>(a, qscale, s);
 }

@@ -628,18 +628,46 @@ void Engine::run_step(const StepView& v, cudaStream_t s) {
   ++launches;
   for (int l = 0; l < arch.n_dec_layers; ++l) {
     const DecL& L = dec[l];
-    gemm(ws.dxa, tc ? &ws.tm_dxa : nullptr, d, L.sqkv, R, ws.dqkv, 3 * d, dt, 0, s);
+    {
+      // q -> ws.dq, this step's k / v straight into the self cache slot t (fused append)
+      GemmArgs g;
+      g.A = ws.dxa;
+      g.lda = d;
+      g.W = L.sqkv.w;
+      g.ldw = L.sqkv.K;
+      g.in_dtype = dt;
+      g.bias = L.sqkv.b;
+      g.M = R;
+      g.N = L.sqkv.N;
+      g.K = L.sqkv.K;
+      g.epi = kEpiQKV;
+      g.C = ws.dq;
+      g.ldc = d;
+      g.c_dtype = dt;
+      g.kc = v.kc[l];
+      g.vc = v.vc[l];
+      g.cap = v.cap;
+      g.seg = d;
+      g.t_ptr = v.t_ptr;
+      g.tmap_a = tc ? &ws.tm_dxa : nullptr;
+      g.tmap_w = tc ? &L.sqkv.tm : nullptr;
+      const int ev = prof_begin(s);
+      CK(launch_gemm(g, s));
+      prof_end(s, ev, gemm_cls, 2.0 * R * L.sqkv.N * L.sqkv.K,
+               (double)R * d * es + (double)L.sqkv.N * L.sqkv.K * es + 3.0 * R * d * es);
+      ++launches;
+    }
     DecAttnArgs a{};
-    a.q = ws.dqkv;
-    a.ldq = 3 * d;
+    a.q = ws.dq;
+    a.ldq = d;
     a.k = v.kc[l];
     a.v = v.vc[l];
     a.ldkv = d;
-    a.k_w = v.kc[l];
-    a.v_w = v.vc[l];
-    a.new_k = (const char*)ws.dqkv + (size_t)d * es;
-    a.new_v = (const char*)ws.dqkv + (size_t)2 * d * es;
-    a.ld_new = 3 * d;
+    a.k_w = nullptr;   // appended by the QKV epilogue
+    a.v_w = nullptr;
+    a.new_k = nullptr;
+    a.new_v = nullptr;
+    a.ld_new = 0;
     a.out = ws.datt;
     a.ldo = d;
     a.dtype = dt;

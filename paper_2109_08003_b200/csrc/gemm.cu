@@ -51,7 +51,20 @@ struct EpiParams {
   int ld_resid;
   unsigned long long* keys;
   TopKPartials tk;
+  void* kc;
+  void* vc;
+  int cap, seg;
+  const int32_t* t_ptr;
 };
+
+// kEpiQKV destination of output element (m, n): q columns go to C, k / v
+// columns to this step's KV-cache slot.
+__device__ __forceinline__ void* qkv_dst(const EpiParams& ep, int m, int n, int t, int es) {
+  const int sec = n / ep.seg, col = n - sec * ep.seg;
+  if (sec == 0) return reinterpret_cast<uint8_t*>(ep.C) + ((size_t)m * ep.ldc + col) * es;
+  uint8_t* cache = reinterpret_cast<uint8_t*>(sec == 1 ? ep.kc : ep.vc);
+  return cache + (((size_t)m * ep.cap + t) * ep.seg + col) * es;
+}
 
 __device__ __forceinline__ float epi_value(const EpiParams& e, int m, int n, float acc) {
   float v = acc;
@@ -62,6 +75,16 @@ __device__ __forceinline__ float epi_value(const EpiParams& e, int m, int n, flo
 }
 
 __device__ __forceinline__ void store_elem(const EpiParams& e, int m, int n, float v) {
+  if (e.epi == kEpiQKV) {
+    void* p = qkv_dst(e, m, n, *e.t_ptr, e.c_dtype == kF32 ? 4 : 2);
+    if (e.c_dtype == kF32)
+      *reinterpret_cast<float*>(p) = v;
+    else if (e.c_dtype == kF16)
+      *reinterpret_cast<__half*>(p) = __float2half_rn(v);
+    else
+      *reinterpret_cast<__nv_bfloat16*>(p) = __float2bfloat16_rn(v);
+    return;
+  }
   size_t off = (size_t)m * e.ldc + n;
   if (e.c_dtype == kF32)
     reinterpret_cast<float*>(e.C)[off] = v;
@@ -94,6 +117,44 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& ep, int m, int n
         best_v = x;
         best_i = nb + i;
       }
+    }
+    return;
+  }
+  if (ep.epi == kEpiQKV) {
+    const int t = *ep.t_ptr;
+    const int es = ep.c_dtype == kF32 ? 4 : 2;
+    const bool one_section = (nb % ep.seg) + 32 <= ep.seg && nb + 32 <= ep.N;
+    if (one_section && es == 2 && (ep.seg % 8) == 0 && (ep.ldc % 8) == 0) {
+      uint32_t packed[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const float a = v[2 * i] + bs[2 * i], b = v[2 * i + 1] + bs[2 * i + 1];
+        if (ep.c_dtype == kF16) {
+          __half2 hh = __floats2half2_rn(a, b);
+          packed[i] = *reinterpret_cast<uint32_t*>(&hh);
+        } else {
+          __nv_bfloat162 hh = __floats2bfloat162_rn(a, b);
+          packed[i] = *reinterpret_cast<uint32_t*>(&hh);
+        }
+      }
+      uint4* dst = reinterpret_cast<uint4*>(qkv_dst(ep, m, nb, t, 2));
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        dst[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
+      return;
+    }
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const int n = nb + i;
+      if (n >= ep.N) continue;
+      const float x = v[i] + bs[i];
+      void* p = qkv_dst(ep, m, n, t, es);
+      if (ep.c_dtype == kF32)
+        *reinterpret_cast<float*>(p) = x;
+      else if (ep.c_dtype == kF16)
+        *reinterpret_cast<__half*>(p) = __float2half_rn(x);
+      else
+        *reinterpret_cast<__nv_bfloat16*>(p) = __float2bfloat16_rn(x);
     }
     return;
   }
@@ -565,7 +626,9 @@ int pick_bn(int M, int N) {
 cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t s) {
   if (g.M <= 0 || g.N <= 0) return cudaSuccess;
   EpiParams ep{g.bias, g.M, g.N, g.epi, g.C, g.ldc, g.c_dtype, g.relu, g.resid, g.ld_resid,
-               g.keys, g.topk};
+               g.keys, g.topk, g.kc, g.vc, g.cap, g.seg, g.t_ptr};
+  if (g.epi == kEpiQKV && (!g.kc || !g.vc || !g.t_ptr || g.seg <= 0 || g.N != 3 * g.seg))
+    return cudaErrorInvalidValue;
   if (g.epi == kEpiTopK && (g.in_dtype == kF32 || (g.topk.K != 4 && g.topk.K != 8)))
     return cudaErrorInvalidValue;   // fp32 path: store logits + launch_logits_topk_partials
   if (g.in_dtype == kF32) {

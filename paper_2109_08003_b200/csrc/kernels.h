@@ -14,6 +14,7 @@ enum Epilogue : int {
   kEpiStore = 0,   // C[m,n] = act(acc + bias[n] (+ resid[m,n]))   in c_dtype
   kEpiArgmax = 1,  // keys[m] = max over n < valid_n of key(acc + bias[n], n)
   kEpiTopK = 2,    // per (row, 256-column tile): max, sum exp(x - max), top-K (value, index)
+  kEpiQKV = 3,     // decoder self q|k|v: q -> C, k / v -> KV cache slot (row*cap + *t_ptr)
 };
 
 // Per-(row, N-tile) partials of the beam epilogue; tile = n / kTopKTile.
@@ -45,6 +46,10 @@ struct GemmArgs {
   int ld_resid = 0;
   unsigned long long* keys = nullptr;  // argmax keys per row (must be pre-zeroed)
   TopKPartials topk{};                 // kEpiTopK outputs
+  void* kc = nullptr;                  // kEpiQKV: self K / V caches [rows*cap, seg]
+  void* vc = nullptr;
+  int cap = 0, seg = 0;
+  const int32_t* t_ptr = nullptr;
   // Pre-encoded TMA descriptors (tcgen05 path).  If null the launcher encodes
   // them on the fly (host cost ~ microseconds).
   const CUtensorMap* tmap_a = nullptr;

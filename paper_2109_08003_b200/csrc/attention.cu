@@ -546,144 +546,6 @@ __global__ void __launch_bounds__(kDThreads) attn_decode_generic(DecAttnArgs a, 
 }
 
 // ---------------------------------------------------------------------------
-// TMA-fed decode attention (16-bit caches, greedy: no ancestor table)
-//
-// CTA = (row, head), NT threads.  Thread 0 streams 2-D TMA boxes of KC keys x
-// BC (= min(dk, 256)) dims through a kStagesT-deep smem ring: first every K
-// chunk (pass 1: scores), then every V chunk (pass 2: weights . V), so the
-// arithmetic keeps the reference order (scores -> softmax -> normalised
-// weights -> value sum).  Each stage holds one chunk laid out [dk/BC][KC][BC].
-
-constexpr int kStagesT = 3;
-
-template <typename T, int NT>
-__global__ void __launch_bounds__(NT)
-    attn_decode_tma_kernel(const __grid_constant__ CUtensorMap tk,
-                           const __grid_constant__ CUtensorMap tv, DecAttnArgs a, float qscale,
-                           int KC, int k_col0, int v_col0) {
-  constexpr int VEC = Vec16<T>::N;
-  extern __shared__ __align__(128) uint8_t smem_t[];
-  const int dk = a.dk;
-  const int BC = dk < 256 ? dk : 256;
-  const int chunk_elems = KC * dk;
-  T* stage_buf = reinterpret_cast<T*>(smem_t);
-  float* qs = reinterpret_cast<float*>(stage_buf + (size_t)kStagesT * chunk_elems);
-  float* S = qs + dk;
-  const int nch = dk / VEC;
-  const int groups = NT / nch;
-  float* red = S + a.max_k + 4;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(
-      (reinterpret_cast<uintptr_t>(red + (size_t)groups * dk) + 7) & ~static_cast<uintptr_t>(7));
-
-  const int r = blockIdx.x, h = blockIdx.y;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const DecCtx c = decode_setup<T>(a, r, h);   // self: appends this step's k/v at slot t
-  const int64_t row0 = a.self_mode ? (int64_t)r * a.cap : c.seq_row0;
-  const int nk = c.nk;
-  const int nchunks = (nk + KC - 1) / KC;
-  const int items = 2 * nchunks;
-  const uint32_t chunk_bytes = (uint32_t)chunk_elems * sizeof(T);
-
-  if (tid == 0) {
-    for (int i = 0; i < kStagesT; ++i) mbar_init(bar + i, 1);
-    fence_mbar_init();
-  }
-  if (a.self_mode) asm volatile("fence.proxy.async.global;" ::: "memory");   // appended k/v -> TMA
-  __syncthreads();
-
-  auto issue = [&](int item) {
-    const int st = item % kStagesT;
-    const bool is_k = item < nchunks;
-    const int ck = is_k ? item : item - nchunks;
-    const CUtensorMap* map = is_k ? &tk : &tv;
-    const int col = (is_k ? k_col0 : v_col0) + h * dk;
-    mbar_expect_tx(bar + st, chunk_bytes);
-    for (int b = 0; b < dk / BC; ++b)
-      tma_load_2d(stage_buf + (size_t)st * chunk_elems + (size_t)b * KC * BC, map, bar + st,
-                  col + b * BC, (int)(row0 + (int64_t)ck * KC));
-  };
-  if (tid == 0)
-    for (int i = 0; i < kStagesT && i < items; ++i) issue(i);
-
-  const T* q = reinterpret_cast<const T*>(a.q) + (size_t)r * a.ldq + h * dk;
-  for (int e = tid; e < dk; e += NT) qs[e] = to_f32(q[e]) * qscale;
-
-  const int ch = tid % nch, grp = tid / nch;
-  float acc[VEC];
-#pragma unroll
-  for (int i = 0; i < VEC; ++i) acc[i] = 0.f;
-
-  for (int item = 0; item < items; ++item) {
-    const int st = item % kStagesT;
-    if (item == nchunks) {   // all scores in S: softmax before the value pass
-      __syncthreads();
-      if (warp == 0) softmax_inplace(S, nk);
-    }
-    mbar_wait(bar + st, (item / kStagesT) & 1);
-    __syncthreads();
-    const T* buf = stage_buf + (size_t)st * chunk_elems;
-    if (item < nchunks) {
-      const int j0 = item * KC;
-      const int jn = min(KC, nk - j0);
-      for (int jj = warp; jj < jn; jj += NT / 32) {
-        float s = 0.f;
-        for (int e0 = lane * VEC; e0 < dk; e0 += 32 * VEC) {
-          float f[VEC];
-          load16(buf + (size_t)(e0 / BC) * KC * BC + (size_t)jj * BC + (e0 % BC), f);
-#pragma unroll
-          for (int i = 0; i < VEC; ++i) s = fmaf(qs[e0 + i], f[i], s);
-        }
-        s = warp_sum(s);
-        if (lane == 0) S[j0 + jj] = c.all_masked ? s + kMaskValue : s;
-      }
-    } else if (grp < groups) {
-      const int j0 = (item - nchunks) * KC;
-      const int jn = min(KC, nk - j0);
-      const int e0 = ch * VEC;
-      const T* col = buf + (size_t)(e0 / BC) * KC * BC + (e0 % BC);
-      for (int jj = grp; jj < jn; jj += groups) {
-        float f[VEC];
-        load16(col + (size_t)jj * BC, f);
-        const float w = S[j0 + jj];
-#pragma unroll
-        for (int i = 0; i < VEC; ++i) acc[i] = fmaf(w, f[i], acc[i]);
-      }
-    }
-    __syncthreads();   // stage consumed
-    if (tid == 0 && item + kStagesT < items) issue(item + kStagesT);
-  }
-  if (grp < groups) {
-#pragma unroll
-    for (int i = 0; i < VEC; ++i) red[grp * dk + ch * VEC + i] = acc[i];
-  }
-  __syncthreads();
-  T* out = reinterpret_cast<T*>(a.out) + (size_t)r * a.ldo + h * dk;
-  for (int e = tid; e < dk; e += NT) {
-    float sum = red[e];
-    for (int gg = 1; gg < groups; ++gg) sum += red[gg * dk + e];
-    out[e] = from_f32<T>(sum);
-  }
-}
-
-template <typename T, int NT>
-cudaError_t launch_dec_tma(const DecAttnArgs& a, const CUtensorMap& tk, const CUtensorMap& tv,
-                           int k_col0, int v_col0, cudaStream_t s) {
-  const int KC = decode_tma_keys_per_chunk(a.dk, a.dtype);
-  const int groups = NT / (a.dk / Vec16<T>::N);
-  size_t smem = (size_t)kStagesT * KC * a.dk * sizeof(T) +
-                sizeof(float) * ((size_t)a.dk + a.max_k + 4 + (size_t)groups * a.dk);
-  smem += 8 * kStagesT + 8;   // mbarriers (+ alignment slack)
-  if (smem > 227 * 1024) return cudaErrorInvalidValue;
-  cudaError_t e = cudaFuncSetAttribute(attn_decode_tma_kernel<T, NT>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  const float qscale = (float)(1.0 / sqrt((double)a.dk));
-  attn_decode_tma_kernel<T, NT><<<dim3(a.rows, a.heads), NT, smem, s>>>(tk, tv, a, qscale, KC,
-                                                                        k_col0, v_col0);
-  return cudaGetLastError();
-}
-
-// ---------------------------------------------------------------------------
 // dispatch
 
 template <typename T>
@@ -793,28 +655,6 @@ cudaError_t launch_attention_decode(const DecAttnArgs& a, cudaStream_t s) {
     case kBF16: return decode_dispatch<__nv_bfloat16>(a, s);
   }
   return cudaErrorInvalidValue;
-}
-
-// ~32 KB per stage: KC keys of dk 16-bit values (multiple of 8, at most 128 keys).
-int decode_tma_keys_per_chunk(int dk, int dtype) {
-  const int es = dtype == kF32 ? 4 : 2;
-  int kc = 32768 / (dk * es);
-  kc = kc > 128 ? 128 : kc;
-  kc = (kc / 8) * 8;
-  return kc < 8 ? 8 : kc;
-}
-
-cudaError_t launch_attention_decode_tma(const DecAttnArgs& a, const CUtensorMap& tk,
-                                        const CUtensorMap& tv, int k_col0, int v_col0,
-                                        cudaStream_t s) {
-  if (a.rows <= 0) return cudaSuccess;
-  if (a.anc || (a.dtype != kF16 && a.dtype != kBF16) || a.dk % 8) return cudaErrorInvalidValue;
-  const bool wide = (int64_t)a.rows * a.heads < 1200;
-  if (a.dtype == kF16)
-    return wide ? launch_dec_tma<__half, 512>(a, tk, tv, k_col0, v_col0, s)
-                : launch_dec_tma<__half, 128>(a, tk, tv, k_col0, v_col0, s);
-  return wide ? launch_dec_tma<__nv_bfloat16, 512>(a, tk, tv, k_col0, v_col0, s)
-              : launch_dec_tma<__nv_bfloat16, 128>(a, tk, tv, k_col0, v_col0, s);
 }
 
 }  // namespace fnmt

@@ -473,11 +473,12 @@ void Engine::reserve(int tok_cap, int row_cap, int64_t pool_cap) {
               make_tmap_16(&ws.tm_dh, ws.dh, dt, row_cap, fd, fd, 128, &err);
     if (!ok) throw EngineError(FNMT_E_CUDA, "workspace TMA descriptor: " + err);
     // decode-attention K/V maps (box = KC keys x min(dk, 256) dims)
-    // Off by default: measured slower than attn_decode_kernel (r01: 79 ms vs 44 ms per 16k
-    // sentences) because the 96 KB stage ring limits residency to 2 CTAs/SM.
+    // Persistent TMA decode attention (decode_attn.cu) is opt-in (FNMT_DECODE_TMA=1): r01
+    // measured 45 ms vs 26 ms (6-1-1) per 16k sentences — per-item consumer latency
+    // (q load, 4 barriers, 1-warp softmax) dominates once the producer runs ahead.
     const int dkd = d / arch.n_heads_dec;
-    ws.kv_tma = getenv("FNMT_DECODE_TMA") != nullptr && dkd % 8 == 0 &&
-                (dkd <= 256 || dkd % 256 == 0);
+    const char* env = getenv("FNMT_DECODE_TMA");
+    ws.kv_tma = env && env[0] == '1' && dkd % 8 == 0 && (dkd <= 256 || dkd % 256 == 0);
     ws.tm_sk.resize(arch.n_dec_layers);
     ws.tm_sv.resize(arch.n_dec_layers);
     ws.tm_ckv.resize(arch.n_dec_layers);

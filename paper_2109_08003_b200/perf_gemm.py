@@ -1,0 +1,63 @@
+"""GEMM shape microbenchmark for the tcgen05 kernel (fnmt_linear), warm L2,
+launches captured in a CUDA graph and timed with CUDA events.
+
+python -m paper_2109_08003_b200.perf_gemm
+"""
+import sys
+
+import torch
+
+from . import _capi
+from ._capi import check, lib, ptr
+
+SHAPES = [  # (M, N, K, note)
+    (600, 512, 512, "dec o-proj, long batch"),
+    (600, 1536, 512, "dec qkv, long batch"),
+    (600, 2048, 512, "dec ffn1, long batch"),
+    (600, 512, 2048, "dec ffn2, long batch"),
+    (2000, 512, 512, "dec o-proj"),
+    (2000, 1536, 512, "dec qkv"),
+    (2000, 2048, 512, "dec ffn1"),
+    (2000, 512, 2048, "dec ffn2"),
+    (3072, 512, 512, "dec o-proj, short batch"),
+    (2000, 32772, 512, "vocab (store f32)"),
+    (64000, 1536, 512, "enc qkv"),
+    (64000, 2048, 512, "enc ffn1"),
+    (64000, 512, 2048, "enc ffn2"),
+]
+
+
+def bench(M, N, K, reps=20, out_dtype=_capi.F16):
+    dev = torch.device("cuda")
+    A = torch.randn(M, K, device=dev).half()
+    W = (torch.randn(N, K, device=dev) / K ** 0.5).half()
+    b = torch.zeros(N, device=dev)
+    C = torch.empty(M, N, device=dev, dtype=torch.float16 if out_dtype == _capi.F16 else torch.float32)
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    torch.cuda.synchronize()
+    with torch.cuda.graph(g, stream=s):
+        for _ in range(reps):
+            check(lib.fnmt_linear(ptr(A), K, _capi.F16, ptr(W), K, ptr(b), ptr(C), N, out_dtype, M, N,
+                                  K, 0, None, 0, s.cuda_stream), "linear")
+    g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(5):
+        g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    us = e0.elapsed_time(e1) * 1e3 / (5 * reps)
+    return us, 2.0 * M * N * K / (us * 1e-6) / 1e12
+
+
+def main():
+    for M, N, K, note in SHAPES:
+        us, tf = bench(M, N, K, out_dtype=_capi.F32 if "f32" in note else _capi.F16)
+        print(f"M={M:6d} N={N:6d} K={K:5d}  {us:8.2f} us  {tf:7.1f} TFLOP/s  {note}")
+    sys.stdout.flush()
+
+
+if __name__ == "__main__":
+    main()

@@ -271,6 +271,8 @@ __device__ __forceinline__ void softmax_inplace(float* S, int nk) {
 // to fill the machine (long-sentence batches).
 template <typename T, int G, int CH, int NT>
 __global__ void __launch_bounds__(NT) attn_decode_kernel(DecAttnArgs a, float qscale) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int VEC = Vec16<T>::N;
   extern __shared__ float sm[];
   const int dk = a.dk;
@@ -388,6 +390,8 @@ __device__ __forceinline__ void smem16(const T* p, float (&f)[Vec16<T>::N]) {
 // G lanes per key, 32/G keys per warp round.
 template <typename T, int G, int CH, int NT>
 __global__ void __launch_bounds__(NT) attn_decode_async_kernel(DecAttnArgs a, float qscale) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int VEC = Vec16<T>::N;
   constexpr int U = 8;                       // warp rounds staged per batch
   constexpr int KPW = 32 / G;
@@ -574,8 +578,8 @@ cudaError_t launch_dec_nt(const DecAttnArgs& a, float qscale, cudaStream_t s) {
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  attn_decode_kernel<T, G, CH, NT><<<dim3(a.rows, a.heads), NT, smem, s>>>(a, qscale);
-  return cudaGetLastError();
+  return launch_k(attn_decode_kernel<T, G, CH, NT>, dim3(a.rows, a.heads), dim3(NT), smem, s, a,
+                  qscale);
 }
 
 template <typename T, int G, int CH, int NT>
@@ -589,8 +593,8 @@ cudaError_t launch_dec_async(const DecAttnArgs& a, float qscale, cudaStream_t s)
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  attn_decode_async_kernel<T, G, CH, NT><<<dim3(a.rows, a.heads), NT, smem, s>>>(a, qscale);
-  return cudaGetLastError();
+  return launch_k(attn_decode_async_kernel<T, G, CH, NT>, dim3(a.rows, a.heads), dim3(NT), smem, s,
+                  a, qscale);
 }
 
 template <typename T, int G, int CH>

@@ -132,6 +132,8 @@ __global__ void logits_topk_partials_kernel(const float* __restrict__ logits, in
 
 // one warp per row: logZ and the row's top-k
 __global__ void beam_row_reduce_kernel(BeamState b) {
+  pdl_trigger();
+  pdl_wait();
   const int r = blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (r >= b.rows || !b.active[r]) return;
@@ -196,6 +198,8 @@ __global__ void beam_select_kernel(BeamState b) {
   __shared__ int sh_par[kWarpsPerCta][KM];
   __shared__ int sh_stop[kWarpsPerCta];
   __shared__ int cta_alive;
+  pdl_trigger();
+  pdl_wait();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int s = blockIdx.x * kWarpsPerCta + warp;
   const int t = *b.t;
@@ -377,13 +381,13 @@ cudaError_t launch_logits_topk_partials(const float* logits, int rows, int n,
 }
 
 cudaError_t launch_beam_row_reduce(const BeamState& b, cudaStream_t s) {
-  beam_row_reduce_kernel<<<(b.rows + kWarpsPerCta - 1) / kWarpsPerCta, 32 * kWarpsPerCta, 0, s>>>(b);
-  return cudaGetLastError();
+  return launch_k(beam_row_reduce_kernel, dim3((b.rows + kWarpsPerCta - 1) / kWarpsPerCta),
+                  dim3(32 * kWarpsPerCta), 0, s, b);
 }
 
 cudaError_t launch_beam_select(const BeamState& b, cudaStream_t s) {
-  beam_select_kernel<<<(b.nS + kWarpsPerCta - 1) / kWarpsPerCta, 32 * kWarpsPerCta, 0, s>>>(b);
-  return cudaGetLastError();
+  return launch_k(beam_select_kernel, dim3((b.nS + kWarpsPerCta - 1) / kWarpsPerCta),
+                  dim3(32 * kWarpsPerCta), 0, s, b);
 }
 
 cudaError_t launch_beam_final(const BeamState& b, cudaStream_t s) {

@@ -70,6 +70,17 @@ __device__ __forceinline__ float warp_max(float v) {
 }
 
 // ---------------------------------------------------------------------------
+// Programmatic dependent launch: kernels launched with the PDL attribute may
+// start while their predecessor drains; every thread calls pdl_wait() before
+// its first access to data the predecessor touches, and pdl_trigger() lets the
+// successor be scheduled early.  Both are no-ops without the attribute.
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// ---------------------------------------------------------------------------
 // shared-memory addressing / mbarrier
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

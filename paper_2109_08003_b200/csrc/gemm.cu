@@ -348,6 +348,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
+  // PDL: barrier init / TMEM alloc / descriptor prefetch above overlap the
+  // predecessor's tail; A (and everything else) is read only after this.
+  pdl_trigger();
+  pdl_wait();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -550,14 +554,22 @@ cudaError_t launch_tc(const CUtensorMap& ta, const CUtensorMap& tw, const GemmAr
   const int tiles = tiles_n * ((g.M + kBM - 1) / kBM);
   const int grid = tiles < num_sms() ? tiles : num_sms();
   const uint32_t idesc = umma_idesc_f16(kBM, BN, g.in_dtype == kBF16);
-  gemm_tc_kernel<BN, STAGES, TOPK><<<grid, kTcThreads, Cfg::kSmem, s>>>(ta, tw, g.K, idesc, ep,
-                                                                        tiles_n, tiles);
-  return cudaGetLastError();
+  return launch_k(gemm_tc_kernel<BN, STAGES, TOPK>, dim3(grid), dim3(kTcThreads),
+                  (size_t)Cfg::kSmem, s, ta, tw, g.K, idesc, ep, tiles_n, tiles);
 }
 
 }  // namespace
 
 int gemm_tile_n() { return kWBox; }
+
+bool pdl_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("FNMT_PDL");
+    on = !(e && e[0] == '0');
+  }
+  return on != 0;
+}
 
 bool make_tmap_16(CUtensorMap* out, const void* base, int dtype, int64_t rows, int64_t cols,
                   int64_t ld, int box_rows, std::string* err) {

@@ -6,8 +6,29 @@
 #include <stdint.h>
 
 #include <string>
+#include <utility>
 
 namespace fnmt {
+
+// Launch with the programmatic-stream-serialization attribute (PDL) unless
+// FNMT_PDL=0.  Kernels launched this way call pdl_wait() before touching
+// their predecessor's data (common.cuh).
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                     Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 // GEMM epilogues: what happens to acc = A[m,:] . W[n,:] (fp32) for each (m, n).
 enum Epilogue : int {

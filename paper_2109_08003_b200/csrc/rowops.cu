@@ -41,6 +41,8 @@ __global__ void embed_kernel(const int32_t* __restrict__ ids, const int32_t* __r
                              const float* __restrict__ table, const float* __restrict__ ptab,
                              float scale, float* __restrict__ x32, TA* __restrict__ xact, int n,
                              int d) {
+  pdl_trigger();
+  pdl_wait();
   const int d4 = d >> 2;
   const int64_t total = (int64_t)n * d4;
   const int pscalar = pos_scalar ? *pos_scalar : 0;
@@ -68,6 +70,8 @@ __global__ void add_norm_kernel(const float* __restrict__ x, const float* __rest
                                 const float* __restrict__ gain, const float* __restrict__ bias,
                                 int l1, float* __restrict__ out32, TA* __restrict__ out_act,
                                 int rows, int d) {
+  pdl_trigger();
+  pdl_wait();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= rows) return;
@@ -138,25 +142,29 @@ cudaError_t add_norm_dispatch(const float* x, const float* y, const float* g, co
   const int threads = 256;
   const int blocks = (int)(((int64_t)rows * 32 + threads - 1) / threads);
   const int nv = (d / 4 + 31) / 32;
+  void (*k)(const float*, const float*, const float*, const float*, int, float*, TA*, int, int) =
+      nullptr;
   if (nv <= 1)
-    add_norm_kernel<TA, 1><<<blocks, threads, 0, s>>>(x, y, g, b, l1, o32, oa, rows, d);
+    k = add_norm_kernel<TA, 1>;
   else if (nv <= 2)
-    add_norm_kernel<TA, 2><<<blocks, threads, 0, s>>>(x, y, g, b, l1, o32, oa, rows, d);
+    k = add_norm_kernel<TA, 2>;
   else if (nv <= 4)
-    add_norm_kernel<TA, 4><<<blocks, threads, 0, s>>>(x, y, g, b, l1, o32, oa, rows, d);
+    k = add_norm_kernel<TA, 4>;
   else if (nv <= 6)
-    add_norm_kernel<TA, 6><<<blocks, threads, 0, s>>>(x, y, g, b, l1, o32, oa, rows, d);
+    k = add_norm_kernel<TA, 6>;
   else if (nv <= 8)
-    add_norm_kernel<TA, 8><<<blocks, threads, 0, s>>>(x, y, g, b, l1, o32, oa, rows, d);
+    k = add_norm_kernel<TA, 8>;
   else if (nv <= 16)
-    add_norm_kernel<TA, 16><<<blocks, threads, 0, s>>>(x, y, g, b, l1, o32, oa, rows, d);
+    k = add_norm_kernel<TA, 16>;
   else
     return cudaErrorInvalidValue;
-  return cudaGetLastError();
+  return launch_k(k, dim3(blocks), dim3(threads), 0, s, x, y, g, b, l1, o32, oa, rows, d);
 }
 
 // Single CTA: every row reads the same step counter, then thread 0 bumps it.
 __global__ void __launch_bounds__(1024) greedy_update_kernel(GreedyState g) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ int alive_s;
   const int t = *g.t;
   if (threadIdx.x == 0) alive_s = 0;
@@ -258,16 +266,13 @@ cudaError_t launch_embed(const int32_t* ids, const int32_t* pos_ids, const int32
   const int threads = 256;
   const int blocks = (int)std::min<int64_t>((total + threads - 1) / threads, 148 * 32);
   if (act_dtype == kF16 || !xact)
-    embed_kernel<__half><<<blocks, threads, 0, s>>>(ids, pos_ids, pos_scalar, table, pos_table,
-                                                    scale, x32, (__half*)xact, n, d);
-  else if (act_dtype == kBF16)
-    embed_kernel<__nv_bfloat16><<<blocks, threads, 0, s>>>(ids, pos_ids, pos_scalar, table,
-                                                           pos_table, scale, x32,
-                                                           (__nv_bfloat16*)xact, n, d);
-  else
-    embed_kernel<float><<<blocks, threads, 0, s>>>(ids, pos_ids, pos_scalar, table, pos_table,
-                                                   scale, x32, (float*)xact, n, d);
-  return cudaGetLastError();
+    return launch_k(embed_kernel<__half>, dim3(blocks), dim3(threads), 0, s, ids, pos_ids,
+                    pos_scalar, table, pos_table, scale, x32, (__half*)xact, n, d);
+  if (act_dtype == kBF16)
+    return launch_k(embed_kernel<__nv_bfloat16>, dim3(blocks), dim3(threads), 0, s, ids, pos_ids,
+                    pos_scalar, table, pos_table, scale, x32, (__nv_bfloat16*)xact, n, d);
+  return launch_k(embed_kernel<float>, dim3(blocks), dim3(threads), 0, s, ids, pos_ids,
+                  pos_scalar, table, pos_table, scale, x32, (float*)xact, n, d);
 }
 
 cudaError_t launch_add_norm(const float* x, const float* y, const float* gain, const float* bias,
@@ -284,8 +289,7 @@ cudaError_t launch_add_norm(const float* x, const float* y, const float* gain, c
 }
 
 cudaError_t launch_greedy_update(const GreedyState& g, cudaStream_t s) {
-  greedy_update_kernel<<<1, 1024, 0, s>>>(g);
-  return cudaGetLastError();
+  return launch_k(greedy_update_kernel, dim3(1), dim3(1024), 0, s, g);
 }
 
 cudaError_t launch_argmax_rows(const float* logits, int ld, int rows, int n, int32_t* out_idx,

@@ -175,6 +175,11 @@ int fnmt_engine_decode_step(fnmt_engine* e, const int32_t* d_prev, int t, int ro
                             const int32_t* d_k_len, int k_pad, int max_k, float* d_logits);
 
 int64_t fnmt_engine_device_bytes(const fnmt_engine* e);
+
+/* Concurrent decode lanes: extra workspaces/streams/graphs sharing the
+ * weights; batches are dealt longest-first / shortest-first across lanes so
+ * latency-bound decode steps overlap.  Default 3 (env FNMT_LANES). */
+int fnmt_engine_set_lanes(fnmt_engine* e, int lanes);
 void* fnmt_engine_stream(fnmt_engine* e);
 
 /* Kernel classes for the per-launch profiler. */

@@ -75,6 +75,7 @@ _SIGNATURES = {
     "fnmt_engine_decode_step": (_I, [_VP, _VP, _I, _I, _I, _VP, _VP, _VP, _VP, _VP, _I, _I,
                                      _VP]),
     "fnmt_engine_device_bytes": (_I64, [_VP]),
+    "fnmt_engine_set_lanes": (_I, [_VP, _I]),
     "fnmt_engine_stream": (_VP, [_VP]),
     "fnmt_engine_profile": (_I, [_VP, _I]),
     "fnmt_engine_profile_read": (_I, [_VP, _VP, _VP, _VP, _VP]),

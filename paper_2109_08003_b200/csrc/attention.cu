@@ -559,8 +559,7 @@ cudaError_t varlen_dispatch(const AttnArgs& a, cudaStream_t s) {
       sizeof(float) * ((size_t)kQT * kcap + (size_t)kDC * (kQT + 4) + (size_t)kDC * (kKT + 4));
   static_assert(kDC * (kKT + 4) >= kPK * (kPD + 4), "V tile must fit in the K tile region");
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
-  cudaError_t e = cudaFuncSetAttribute(attn_varlen_kernel<T>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = set_max_smem((const void*)attn_varlen_kernel<T>);
   if (e != cudaSuccess) return e;
   dim3 grid((a.max_q + kQT - 1) / kQT, a.n_seq, a.heads);
   const float qscale = (float)(1.0 / sqrt((double)a.dk));
@@ -574,8 +573,7 @@ cudaError_t launch_dec_nt(const DecAttnArgs& a, float qscale, cudaStream_t s) {
   const size_t smem = sizeof(float) * ((size_t)a.dk + a.max_k + 4 + (size_t)groups * a.dk);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(attn_decode_kernel<T, G, CH, NT>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = set_max_smem((const void*)attn_decode_kernel<T, G, CH, NT>);
     if (e != cudaSuccess) return e;
   }
   return launch_k(attn_decode_kernel<T, G, CH, NT>, dim3(a.rows, a.heads), dim3(NT), smem, s, a,
@@ -589,8 +587,7 @@ cudaError_t launch_dec_async(const DecAttnArgs& a, float qscale, cudaStream_t s)
                       sizeof(float) * ((size_t)a.dk + a.max_k + 4 + (size_t)NW * a.dk);
   if (smem > 227 * 1024) return launch_dec_nt<T, G, CH, NT>(a, qscale, s);
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(attn_decode_async_kernel<T, G, CH, NT>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = set_max_smem((const void*)attn_decode_async_kernel<T, G, CH, NT>);
     if (e != cudaSuccess) return e;
   }
   return launch_k(attn_decode_async_kernel<T, G, CH, NT>, dim3(a.rows, a.heads), dim3(NT), smem, s,
@@ -631,8 +628,7 @@ cudaError_t decode_dispatch(const DecAttnArgs& a, cudaStream_t s) {
   const size_t smem = sizeof(float) * ((size_t)a.dk + (size_t)a.max_k + 32);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(attn_decode_generic<T>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = set_max_smem((const void*)attn_decode_generic<T>);
     if (e != cudaSuccess) return e;
   }
   attn_decode_generic<T><<<dim3(a.rows, a.heads), kDThreads, smem, s>>>(a, qscale);

@@ -375,7 +375,15 @@ int fnmt_engine_profile_read(fnmt_engine* e, double* ms, int64_t* launches, doub
   return FNMT_OK;
 }
 
-int64_t fnmt_engine_device_bytes(const fnmt_engine* e) { return e ? e->eng->device_bytes : 0; }
+int64_t fnmt_engine_device_bytes(const fnmt_engine* e) {
+  return e ? e->eng->total_device_bytes() : 0;
+}
+
+int fnmt_engine_set_lanes(fnmt_engine* e, int lanes) {
+  if (!e || lanes < 1 || lanes > 16) return fail(FNMT_E_INVALID, "set_lanes: 1..16");
+  e->eng->n_lanes = lanes;
+  return FNMT_OK;
+}
 
 void* fnmt_engine_stream(fnmt_engine* e) { return e ? (void*)e->eng->stream : nullptr; }
 

@@ -257,8 +257,7 @@ cudaError_t launch_persist(const DecAttnArgs& a, const CUtensorMap& tk, const CU
                       sizeof(float) * ((size_t)a.dk + a.max_k + 4 + (size_t)groups * a.dk) + 8 +
                       16 * NST;
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
-  cudaError_t e = cudaFuncSetAttribute(attn_decode_persist_kernel<T, NST>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = set_max_smem((const void*)attn_decode_persist_kernel<T, NST>);
   if (e != cudaSuccess) return e;
   const int items = a.rows * a.heads;
   const int grid = items < num_sms_attn() ? items : num_sms_attn();

@@ -182,6 +182,8 @@ Engine::Engine(const fnmt_arch& a, int device, int dtype) : arch(a), device(devi
   CK(cudaEventCreateWithFlags(&ev_poll[1], cudaEventDisableTiming));
   CK(cudaEventCreate(&ev_t0));
   CK(cudaEventCreate(&ev_t1));
+  CK(cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming));
+  if (const char* e = getenv("FNMT_LANES")) n_lanes = std::max(1, atoi(e));
   CK(cudaHostAlloc(&h_alive, 4 * sizeof(int32_t), cudaHostAllocDefault));
 }
 
@@ -231,6 +233,8 @@ void Engine::prof_collect() {
 }
 
 Engine::~Engine() {
+  lanes.clear();   // lanes share this engine's weights
+  if (ev_done) cudaEventDestroy(ev_done);
   for (cudaEvent_t e : prof_events) cudaEventDestroy(e);
   cudaSetDevice(device);
   if (graph_exec) cudaGraphExecDestroy(graph_exec);
@@ -845,16 +849,115 @@ void Engine::translate_device(const int32_t* d_ids, const int64_t* d_off,
       // tiny synchronous-order write via the stream
       CK(cudaMemsetAsync(d_out_len + i, 0, sizeof(int32_t), stream));
     }
-  int64_t steps_total = 0, tgt_capacity = 0;
-  for (size_t bi = 0; bi < plan.size(); ++bi) {
-    const Batch& b = plan[bi];
+  PlanCtx P{plan, live_len, budget_all, batch_row0, batch_cu0, meta_perm, meta_cu, meta_budget,
+            d_ids, d_off, d_out_ids, d_out_off, d_out_len, run};
+  int64_t steps_total = 0;
+  // Lanes: extra engines sharing these weights, each with its own workspace,
+  // stream and decode graph.  Batches are dealt longest-first to this engine
+  // and shortest-first to the others, so a latency-bound long-sentence decode
+  // (few rows, many steps) overlaps with short-sentence batches.
+  const int want_lanes = profiling ? 1 : std::min<int>(n_lanes, (int)plan.size());
+  if (want_lanes <= 1) {
+    for (size_t bi = 0; bi < plan.size(); ++bi) steps_total += run_batch(P, bi);
+  } else {
+    while ((int)lanes.size() < want_lanes - 1) lanes.push_back(make_lane());
+    std::vector<Engine*> eng{this};
+    for (int i = 0; i < want_lanes - 1; ++i) {
+      Engine* L = lanes[i].get();
+      L->reserve(ws.tok_cap, ws.row_cap, ws.pool_cap);
+      if (kb > 1) L->reserve_beam(beam.sent_cap, beam.k, beam.pool_cap);
+      eng.push_back(L);
+    }
+    cudaEvent_t ready;
+    CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    CK(cudaEventRecord(ready, stream));
+    for (size_t i = 1; i < eng.size(); ++i) CK(cudaStreamWaitEvent(eng[i]->stream, ready, 0));
+    std::mutex mu;
+    int front = 0, back = (int)plan.size() - 1;
+    std::vector<int64_t> steps(eng.size(), 0), l0(eng.size());
+    std::vector<std::exception_ptr> errs(eng.size());
+    for (size_t i = 0; i < eng.size(); ++i) l0[i] = eng[i]->launches;
+    std::vector<std::thread> th;
+    for (size_t i = 0; i < eng.size(); ++i) {
+      th.emplace_back([&, i] {
+        try {
+          CK(cudaSetDevice(device));
+          for (;;) {
+            int bi;
+            {
+              std::lock_guard<std::mutex> g(mu);
+              if (front > back) break;
+              bi = i == 0 ? front++ : back--;
+            }
+            steps[i] += eng[i]->run_batch(P, (size_t)bi);
+          }
+        } catch (...) {
+          errs[i] = std::current_exception();
+        }
+      });
+    }
+    for (auto& t : th) t.join();
+    for (size_t i = 1; i < eng.size(); ++i) {
+      CK(cudaEventRecord(eng[i]->ev_done, eng[i]->stream));
+      CK(cudaStreamWaitEvent(stream, eng[i]->ev_done, 0));
+      launches += eng[i]->launches - l0[i];
+    }
+    cudaEventDestroy(ready);
+    for (auto& e : errs)
+      if (e) std::rethrow_exception(e);
+    for (int64_t s : steps) steps_total += s;
+  }
+  CK(cudaEventRecord(ev_t1, stream));
+  CK(cudaStreamSynchronize(stream));
+  if (profiling) prof_collect();
+  if (st) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ev_t0, ev_t1);
+    st->sentences += n;
+    int64_t src = 0;
+    for (int32_t L : lengths) src += L;
+    st->source_tokens += src;
+    st->batches += (int64_t)plan.size();
+    st->decode_steps += steps_total;
+    st->gpu_launches += launches - launches0;
+    st->total_ms += ms;
+    st->device_bytes = device_bytes;
+    for (auto& L : lanes) st->device_bytes += L->device_bytes;
+  }
+}
+
+std::unique_ptr<Engine> Engine::make_lane() {
+  std::unique_ptr<Engine> L(new Engine(arch, device, dt));
+  L->src_emb32 = src_emb32;
+  L->tgt_emb32 = tgt_emb32;
+  L->pos32 = pos32;
+  L->out = out;
+  L->enc = enc;
+  L->dec = dec;
+  L->finalized = true;   // weights are shared (owned by this engine)
+  L->n_lanes = 1;
+  return L;
+}
+
+// One planned batch on this engine's workspace / stream: gather -> encode ->
+// decode (greedy or beam) -> scatter to the sentence slots.
+int64_t Engine::run_batch(const PlanCtx& P, size_t bi) {
+  const Batch& b = P.plan[bi];
+  const fnmt_run& run = P.run;
+  const int32_t* d_ids = P.d_ids;
+  const int64_t* d_off = P.d_off;
+  int32_t* d_out_ids = P.d_out_ids;
+  const int64_t* d_out_off = P.d_out_off;
+  int32_t* d_out_len = P.d_out_len;
+  int64_t steps_total = 0;
+  {
     const int R = (int)b.rows.size();
-    const int32_t* perm_b = meta_perm + batch_row0[bi];
-    const int32_t* cu_b = meta_cu + batch_cu0[bi];
+    const int32_t* perm_b = P.meta_perm + P.batch_row0[bi];
+    const int32_t* cu_b = P.meta_cu + P.batch_cu0[bi];
     int n_tok = 0, cap = 0;
     for (int r = 0; r < R; ++r) {
-      n_tok += live_len[b.rows[r]];
-      cap = std::max(cap, budget_all[batch_row0[bi] + r]);
+      n_tok += P.live_len[b.rows[r]];
+      cap = std::max(cap, P.budget_all[P.batch_row0[bi] + r]);
     }
     // 1) gather this batch's source ids into the packed workspace
     int ev = prof_begin(stream);
@@ -864,7 +967,7 @@ void Engine::translate_device(const int32_t* d_ids, const int64_t* d_off,
     ++launches;
     // per-sequence tables: q/k start = cu, len = cu diff
     CK(cudaMemcpyAsync(ws.cu, cu_b, sizeof(int32_t) * (R + 1), cudaMemcpyDeviceToDevice, stream));
-    CK(cudaMemcpyAsync(ws.budget, meta_budget + batch_row0[bi], sizeof(int32_t) * R,
+    CK(cudaMemcpyAsync(ws.budget, P.meta_budget + P.batch_row0[bi], sizeof(int32_t) * R,
                        cudaMemcpyDeviceToDevice, stream));
     lens_from_cu(R);
     // 2) encoder (packed varlen: only real tokens are rows)
@@ -892,24 +995,8 @@ void Engine::translate_device(const int32_t* d_ids, const int64_t* d_off,
     CK(cudaGetLastError());
     prof_end(stream, ev, FNMT_K_OTHER, 0.0, (double)R * cap * 8);
     ++launches;
-    tgt_capacity += n_tok;
   }
-  CK(cudaEventRecord(ev_t1, stream));
-  CK(cudaStreamSynchronize(stream));
-  if (profiling) prof_collect();
-  if (st) {
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, ev_t0, ev_t1);
-    st->sentences += n;
-    int64_t src = 0;
-    for (int32_t L : lengths) src += L;
-    st->source_tokens += src;
-    st->batches += (int64_t)plan.size();
-    st->decode_steps += steps_total;
-    st->gpu_launches += launches - launches0;
-    st->total_ms += ms;
-    st->device_bytes = device_bytes;
-  }
+  return steps_total;
 }
 
 // Replay the captured step (or, when profiling, launch `direct(t)`) for up to

@@ -543,13 +543,9 @@ template <int BN, int STAGES, int TOPK = 0>
 cudaError_t launch_tc(const CUtensorMap& ta, const CUtensorMap& tw, const GemmArgs& g,
                       const EpiParams& ep, cudaStream_t s) {
   using Cfg = TcCfg<BN, STAGES>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<BN, STAGES, TOPK>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static_assert(Cfg::kSmem <= 227 * 1024, "GEMM stage ring exceeds shared memory");
+  cudaError_t e = set_max_smem((const void*)gemm_tc_kernel<BN, STAGES, TOPK>);
+  if (e != cudaSuccess) return e;
   const int tiles_n = (g.N + BN - 1) / BN;
   const int tiles = tiles_n * ((g.M + kBM - 1) / kBM);
   const int grid = tiles < num_sms() ? tiles : num_sms();

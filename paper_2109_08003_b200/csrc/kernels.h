@@ -5,10 +5,26 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
+#include <set>
 #include <string>
 #include <utility>
 
 namespace fnmt {
+
+// Opt a kernel into the full 227 KB of dynamic shared memory once (thread
+// safe: decode lanes launch the same kernels from several host threads, and a
+// per-launch attribute would race with another thread's launch).
+inline cudaError_t set_max_smem(const void* func) {
+  static std::mutex mu;
+  static std::set<const void*> done;
+  std::lock_guard<std::mutex> g(mu);
+  if (done.count(func)) return cudaSuccess;
+  cudaError_t e =
+      cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  if (e == cudaSuccess) done.insert(func);
+  return e;
+}
 
 // Launch with the programmatic-stream-serialization attribute (PDL) unless
 // FNMT_PDL=0.  Kernels launched this way call pdl_wait() before touching

@@ -14,16 +14,19 @@ __version__ = "0.1.0"
 
 __all__ = ["ModelConfig", "Weights", "count_params", "random_model", "sinusoid_positions",
            "tensor_manifest", "PAD_ID", "UNK_ID", "BOS_ID", "EOS_ID", "GpuTranslationModel",
-           "Engine", "RunConfig", "greedy_translate", "beam_translate", "SearchConfig"]
+           "Engine", "RunConfig", "Translator", "greedy_translate", "beam_translate", "SearchConfig"]
 
 
 def __getattr__(name):
     if name in ("GpuTranslationModel", "GpuEncoderOutput", "GpuDecodeCache", "LengthError"):
         from . import model
         return getattr(model, name)
-    if name in ("Engine", "RunConfig"):
+    if name == "Engine":
         from . import engine
-        return getattr(engine, name)
+        return engine.Engine
+    if name in ("Translator", "RunConfig"):
+        from . import translator
+        return getattr(translator, name)
     if name in ("greedy_translate", "beam_translate", "SearchConfig", "max_out_length"):
         from . import search
         return getattr(search, name)

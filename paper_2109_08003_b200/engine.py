@@ -10,14 +10,14 @@ one native call.  Two entry points, matching the two halves of the bench:
   the host<->device copies happen inside the call (the ``e2e`` path);
 * :meth:`Engine.translate_device` — inputs and outputs already in HBM.
 
-``RunConfig`` mirrors the reference's run flags (cli.py:20-45) with the GPU
-decoding caps of the paper (sbatch 3072 / wbatch 64000).
+``RunConfig`` (defined in ``translator.py``) mirrors the reference's run
+flags (cli.py:20-45) with the GPU decoding caps of the paper (sbatch 3072 /
+wbatch 64000).
 """
 
 from __future__ import annotations
 
 import ctypes as C
-from dataclasses import dataclass
 
 import numpy as np
 import torch
@@ -25,19 +25,7 @@ import torch
 from . import _capi
 from ._capi import check, lib, ptr
 from .store import BOS_ID, EOS_ID, PAD_ID
-
-
-@dataclass(frozen=True)
-class RunConfig:
-    precision: str = "f16"          # f16 / bf16 / f32 (parity mode)
-    sbatch: int = 3072
-    wbatch: int = 64000
-    workers: int = 1                # GPUs (one process each; see bench.py)
-    chunk_lines: int = 2000
-    beam: int = 1
-    pretokenized: bool = False
-    max_len_ratio: float = 1.5
-    max_len_offset: int = 5
+from .translator import RunConfig  # noqa: F401  (re-export; cli.py:34-45)
 
 
 def run_struct(sbatch, wbatch, ratio=1.5, offset=5, beam=1, bos=BOS_ID, eos=EOS_ID,

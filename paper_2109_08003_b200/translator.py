@@ -1,0 +1,263 @@
+"""``Translator`` / ``RunConfig``: the reference's text-level translate and
+bench entry points on the B200 engine.
+
+The reference ``fastnmt.engine`` module is missing upstream;
+its contract is reconstructed from its callers — ``cli.py:34-89``,
+``tests/test_engine_cli.py:21-145``, ``tests/test_acceptance.py:408-455``
+and SPEC.md:593-650:
+
+* ``Translator(cfg, weights, vocab, codec=None, run=RunConfig())``,
+  ``Translator.from_file(path, run=, bpe_codes=)``, ``.codec`` assignable;
+* ``translate_lines(lines)``: tokenize -> BPE -> id-map -> (sort/batch ->
+  decode on the GPU) -> id-unmap -> BPE-join -> detokenize; line count
+  preserved, empty line -> empty line, over-long lines hard-split at
+  ``min(1024, max_positions)`` subword tokens and rejoined;
+* ``bench(lines)``: ``words_per_second`` = source words / wall seconds plus
+  the configured limits, and the GPU-side target-word rate;
+* ``selftest()``: the dirty-data / empty / over-long battery.
+
+B200 design: the text stages are host work on ``run.workers`` threads, the
+GPU stage is one native ``fnmt_engine_translate`` call per group of chunks
+(length-sorted token-budget batching, graph-captured decode, order restore
+inside the call).  The three stages are pipelined — chunk i+1 is tokenized
+and chunk i-1 detokenized while the engine call for chunk i runs (ctypes
+releases the GIL for the native call).  Because every engine kernel is
+batch-invariant, the output does not depend on ``workers``,
+``chunk_lines``, ``sbatch`` or ``wbatch`` (the reference's worker- and
+cap-invariance contracts, test_engine_cli.py:39-55).
+"""
+
+from __future__ import annotations
+
+import time
+from concurrent.futures import ThreadPoolExecutor
+from dataclasses import dataclass, replace
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import modelfile
+from .store import ModelConfig, config_of
+from .textpipe import (BOS_ID, EOS_ID, PAD_ID, BpeCodec, ChunkFailure, Vocabulary, bpe_decode,
+                       bpe_encode, detokenize, tokenize)
+
+PRECISIONS = ("f32", "f16", "bf16", "int8")
+HARD_SPLIT = 1024            # SPEC.md:369 default hard limit (BPE tokens)
+GPU_GROUP_LINES = 65536      # lines per engine call when the result is batch-invariant
+
+
+@dataclass(frozen=True)
+class RunConfig:
+    """Run flags (cli.py:20-45).  Defaults are the paper's GPU decoding
+    configuration (sbatch/wbatch 3072/64000) and the fp16
+    production precision; ``precision="f32"`` is the bit-faithful parity mode
+    and ``"int8"`` the per-column quantized GEMM path (quant8.py)."""
+
+    precision: str = "f16"
+    sbatch: int = 3072
+    wbatch: int = 64000
+    workers: int = 1
+    chunk_lines: int = 2000
+    beam: int = 1
+    pretokenized: bool = False
+    max_len_ratio: float = 1.5
+    max_len_offset: int = 5
+
+    def __post_init__(self):
+        if self.precision not in PRECISIONS:
+            raise ValueError(f"unknown precision {self.precision!r}")
+        for name in ("sbatch", "wbatch", "workers", "chunk_lines", "beam"):
+            if getattr(self, name) < 1:
+                raise ValueError(f"{name} must be >= 1")
+
+
+@dataclass
+class _Chunk:
+    pieces: list          # list[np.ndarray int32] subword ids, each <= limit
+    owner: list           # piece -> line index within the chunk
+    n_lines: int
+
+
+class Translator:
+    def __init__(self, cfg, weights, vocab: Vocabulary, codec: Optional[BpeCodec] = None,
+                 run: RunConfig = RunConfig(), device: int = 0):
+        from .engine import Engine
+        self.cfg: ModelConfig = config_of(cfg)
+        if len(vocab) != self.cfg.vocab_size:
+            raise ValueError(f"vocabulary has {len(vocab)} entries, config says "
+                             f"{self.cfg.vocab_size}")
+        self.vocab = vocab
+        self.codec = codec
+        self.run = run
+        self.weights = weights
+        self.engine = Engine(self.cfg, weights, dtype=run.precision, device=device)
+        self.limit = max(1, min(HARD_SPLIT, self.cfg.max_positions))
+
+    @classmethod
+    def from_file(cls, path, run: RunConfig = RunConfig(), bpe_codes=None,
+                  device: int = 0) -> "Translator":
+        cfg, w, vocab = modelfile.load(path, "int8" if run.precision == "int8" else "f32")
+        codec = BpeCodec.load(bpe_codes) if bpe_codes else None
+        return cls(cfg, w, vocab, codec=codec, run=run, device=device)
+
+    def with_run(self, **changes) -> "Translator":
+        """Same engine (weights stay in HBM), different run flags."""
+        t = object.__new__(Translator)
+        t.__dict__.update(self.__dict__)
+        new = replace(self.run, **changes)
+        if new.precision != self.run.precision:
+            raise ValueError("precision is fixed at construction (weights are uploaded once)")
+        t.run = new
+        return t
+
+    # ---- host stages -------------------------------------------------------
+    def _to_ids(self, lines: Sequence[str]) -> _Chunk:
+        pieces, owner = [], []
+        enc = self.vocab.encode
+        for li, line in enumerate(lines):
+            toks = line.split() if self.run.pretokenized else tokenize(line)
+            if self.codec is not None:
+                toks = bpe_encode(toks, self.codec)
+            ids = np.asarray(enc(toks), dtype=np.int32)
+            for s in range(0, len(ids), self.limit):
+                pieces.append(ids[s:s + self.limit])
+                owner.append(li)
+        return _Chunk(pieces, owner, len(lines))
+
+    def _to_text(self, chunk: _Chunk, outs: list) -> list:
+        per_line = [[] for _ in range(chunk.n_lines)]
+        tok = self.vocab.token_of
+        for li, ids in zip(chunk.owner, outs):
+            per_line[li].extend(tok(int(i)) for i in ids)
+        res = []
+        for sub in per_line:
+            words = bpe_decode(sub) if self.codec is not None else sub
+            res.append(" ".join(words) if self.run.pretokenized else detokenize(words))
+        return res
+
+    # ---- GPU stage -----------------------------------------------------------
+    def _translate_pieces(self, pieces: list) -> list:
+        n = len(pieces)
+        if n == 0:
+            return []
+        lengths = np.fromiter((len(p) for p in pieces), dtype=np.int64, count=n)
+        offsets = np.zeros(n + 1, dtype=np.int64)
+        np.cumsum(lengths, out=offsets[1:])
+        ids = np.concatenate(pieces).astype(np.int32) if offsets[-1] else np.zeros(1, np.int32)
+        r = self.run
+        out_ids, out_len, out_off, _ = self.engine.translate(
+            ids, offsets, sbatch=r.sbatch, wbatch=r.wbatch, ratio=r.max_len_ratio,
+            offset=r.max_len_offset, beam=r.beam)
+        return [out_ids[o:o + L] for o, L in zip(out_off.tolist(), out_len.tolist())]
+
+    def _groups(self, n_lines: int) -> list:
+        """Engine-call groups of whole chunks.  int8 quantizes activations per
+        GEMM call over the whole batch (quant8.py:171-195), so its batches are
+        kept inside one chunk — the chunk is the unit the reference's worker
+        invariance is defined on; the float paths are batch-invariant and
+        coalesce chunks into large GPU groups."""
+        step = self.run.chunk_lines
+        per = 1 if self.run.precision == "int8" else max(1, GPU_GROUP_LINES // step)
+        bounds = [(s, min(s + step, n_lines)) for s in range(0, n_lines, step)]
+        return [bounds[i:i + per] for i in range(0, len(bounds), per)]
+
+    def translate_lines(self, lines: Sequence[str]) -> list:
+        lines = list(lines)
+        if not lines:
+            return []
+        groups = self._groups(len(lines))
+        out: list = []
+        with ThreadPoolExecutor(max_workers=self.run.workers) as pool:
+            def prep(group):
+                return [pool.submit(self._to_ids, lines[s:e]) for s, e in group]
+
+            pending_pre = prep(groups[0])
+            pending_post = []
+            for gi, group in enumerate(groups):
+                chunks = []
+                for ci, f in enumerate(pending_pre):
+                    try:
+                        chunks.append(f.result())
+                    except Exception as exc:   # noqa: BLE001
+                        raise ChunkFailure(gi, exc) from exc
+                if gi + 1 < len(groups):
+                    pending_pre = prep(groups[gi + 1])      # overlaps the engine call
+                flat = [p for c in chunks for p in c.pieces]
+                res = self._translate_pieces(flat)
+                k = 0
+                for c in chunks:
+                    pending_post.append(pool.submit(self._to_text, c, res[k:k + len(c.pieces)]))
+                    k += len(c.pieces)
+            for f in pending_post:
+                out.extend(f.result())
+        if len(out) != len(lines):
+            raise ChunkFailure(0, ValueError(f"{len(out)} lines out for {len(lines)} in"))
+        return out
+
+    # ---- bench / selftest ----------------------------------------------------
+    def bench(self, lines: Sequence[str]) -> dict:
+        lines = list(lines)
+        self.engine.handle  # noqa: B018  (engine built in __init__)
+        t0 = time.perf_counter()
+        out = self.translate_lines(lines)
+        wall = time.perf_counter() - t0
+        src_words = sum(len(x.split()) for x in lines)
+        tgt_words = sum(len(x.split()) for x in out)
+        wall = max(wall, 1e-9)
+        return {
+            "words_per_second": src_words / wall,
+            "wall_seconds": wall,
+            "source_words": src_words,
+            "source_sentences": len(lines),
+            "output_lines": len(out),
+            "target_words": tgt_words,
+            "target_words_per_second": tgt_words / wall,
+            "sentences_per_second": len(lines) / wall,
+            "est_peak_bytes": int(self.engine.device_bytes()),
+            "sbatch": self.run.sbatch,
+            "wbatch": self.run.wbatch,
+            "workers": self.run.workers,
+            "chunk_lines": self.run.chunk_lines,
+            "precision": self.run.precision,
+            "beam": self.run.beam,
+            "device": "cuda",
+        }
+
+    def selftest(self) -> list:
+        """(name, ok, detail) per case (test_acceptance.py:445-455)."""
+        rng = np.random.default_rng(0)
+        dirty = bytes(rng.integers(0, 256, size=4096, dtype=np.uint8)).decode(
+            "utf-8", errors="replace").replace("\n", " ")
+        long_line = ("the quick brown fox jumps over the lazy dog " * 2400)[:100_000]
+        cases = [
+            ("empty_input", [], lambda o: o == []),
+            ("empty_lines", ["", "", ""], lambda o: o == ["", "", ""]),
+            ("whitespace_only", ["   \t  "], lambda o: len(o) == 1),
+            ("dirty_bytes", [dirty], lambda o: len(o) == 1),
+            ("control_chars", ["a\x00b\x07c\x1b[31m d"], lambda o: len(o) == 1),
+            ("unknown_words", ["zzz qqq \U0001F600 中文"], lambda o: len(o) == 1),
+            ("very_long_line", [long_line, "short"], lambda o: len(o) == 2 and o[0] != ""),
+            ("mixed_batch", ["one", "", "two three", "x" * 3000, ""],
+             lambda o: len(o) == 5 and o[1] == "" and o[4] == ""),
+        ]
+        results = []
+        for name, lines, ok_fn in cases:
+            try:
+                out = self.translate_lines(lines)
+                ok = bool(ok_fn(out))
+                detail = f"lines_in={len(lines)} lines_out={len(out)}"
+            except Exception as exc:   # noqa: BLE001 - the battery reports, never raises
+                ok, detail = False, f"{type(exc).__name__}: {exc}"
+            results.append((name, ok, detail))
+        try:
+            probe = ["the quick fox", "lazy dog."] * 8
+            a = self.translate_lines(probe)
+            b = self.with_run(workers=self.run.workers + 3).translate_lines(probe)
+            results.append(("worker_invariance", a == b, f"{sum(x == y for x, y in zip(a, b))}"
+                                                         f"/{len(a)} identical"))
+        except Exception as exc:   # noqa: BLE001
+            results.append(("worker_invariance", False, f"{type(exc).__name__}: {exc}"))
+        return results
+
+
+__all__ = ["RunConfig", "Translator", "PRECISIONS", "BOS_ID", "EOS_ID", "PAD_ID"]

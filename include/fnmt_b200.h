@@ -14,7 +14,9 @@
  *     and a cudaStream_t passed as void*, are stream-ordered, non-blocking,
  *     allocation-free and CUDA-graph capturable;
  *   - engine calls own their device memory and stream.
- * dtype codes: 0 = f32, 1 = f16, 2 = bf16.
+ * dtype codes: 0 = f32, 1 = f16, 2 = bf16; engines also take 3 = int8
+ * (f32 activations, per-column int8 GEMM weights: the reference's int8
+ * precision, store.py:29-36 / quant8.py).
  */
 #ifndef FNMT_B200_H
 #define FNMT_B200_H
@@ -83,6 +85,18 @@ int fnmt_linear_argmax(const void* A, int lda, int a_dtype, const void* W, int l
                        const float* bias, int M, int N, int K, uint64_t* keys_scratch,
                        int32_t* out_idx, void* stream);
 
+/* int8 projection: C = f32(qgemm(quantize_activations(A), W)) + bias — the
+ * packed-int8 branch of Projection.apply (model.py:84-90 -> quant8.py:171-195,
+ * :246-278) on tcgen05 kind::i8.  A: f32 [M, K] (lda).  Wq: s8 W^T [N, Kp]
+ * K-major, Kp = K rounded up to 16, zero padded; scale / zp: per-column f32
+ * (quant8.QuantizedMatrix.col_scale / col_zeropoint); colsum: s32 per-column
+ * sum of the K real levels.  workspace: fnmt_qgemm_workspace(M, K) device
+ * bytes.  Bit-identical to the reference's qgemm + bias in f32. */
+int64_t fnmt_qgemm_workspace(int64_t M, int K);
+int fnmt_qgemm(const float* A, int lda, const int8_t* Wq, const float* scale, const float* zp,
+               const int32_t* colsum, const float* bias, float* C, int ldc, int M, int N, int K,
+               int relu, void* workspace, int64_t workspace_bytes, void* stream);
+
 /* x = table[ids] * scale + pos_table[pos_ids]  (model.py:276-277) */
 int fnmt_embed(const int32_t* ids, const int32_t* pos_ids, const float* table,
                const float* pos_table, float scale, float* out32, void* out_act, int act_dtype,
@@ -121,6 +135,13 @@ void fnmt_engine_destroy(fnmt_engine* e);
  * the reference orientation: gemm weights [k, n] (x @ W), out_proj [vocab, d]
  * (aliases src_embed when shared; may be omitted then). */
 int fnmt_engine_set_tensor(fnmt_engine* e, const char* name, const float* host, int64_t numel);
+
+/* int8 engines (dtype 3): a quantized GEMM weight by manifest name (or
+ * "out_proj" as the [d, vocab] projection) in the reference orientation —
+ * q s8 [k, n] row-major with per-column scale / zeropoint, exactly
+ * quant8.QuantizedMatrix (quant8.py:74-82, store.py:337-361). */
+int fnmt_engine_set_qtensor(fnmt_engine* e, const char* name, const int8_t* q, const float* scale,
+                            const float* zp, int64_t k, int64_t n);
 
 /* Validate, pre-transpose to K-major, cast, upload ("extract the transpose
  * operations to the beginning of decoding"). */

@@ -13,8 +13,8 @@ from pathlib import Path
 LIB_PATH = Path(__file__).resolve().parent / "libfnmt_b200.so"
 
 FNMT_OK, FNMT_E_INVALID, FNMT_E_CUDA, FNMT_E_LENGTH, FNMT_E_STATE = 0, -1, -2, -3, -4
-F32, F16, BF16 = 0, 1, 2
-DTYPES = {"f32": F32, "fp32": F32, "f16": F16, "fp16": F16, "bf16": BF16}
+F32, F16, BF16, INT8 = 0, 1, 2, 3
+DTYPES = {"f32": F32, "fp32": F32, "f16": F16, "fp16": F16, "bf16": BF16, "int8": INT8}
 
 
 class fnmt_arch(C.Structure):
@@ -54,6 +54,9 @@ _SIGNATURES = {
     "fnmt_version": (C.c_char_p, []),
     "fnmt_linear": (_I, [_VP, _I, _I, _VP, _I, _VP, _VP, _I, _I, _I, _I, _I, _I, _VP, _I, _VP]),
     "fnmt_linear_argmax": (_I, [_VP, _I, _I, _VP, _I, _VP, _I, _I, _I, _VP, _VP, _VP]),
+    "fnmt_qgemm_workspace": (_I64, [_I64, _I]),
+    "fnmt_qgemm": (_I, [_VP, _I, _VP, _VP, _VP, _VP, _VP, _VP, _I, _I, _I, _I, _I, _VP, _I64,
+                        _VP]),
     "fnmt_embed": (_I, [_VP, _VP, _VP, _VP, _F, _VP, _VP, _I, _I, _I, _VP]),
     "fnmt_add_norm": (_I, [_VP, _VP, _VP, _VP, _I, _VP, _VP, _I, _I, _I, _VP]),
     "fnmt_attention": (_I, [_VP, _I, _VP, _VP, _I, _VP, _I, _I, _I, _I, _VP, _VP, _VP, _VP,
@@ -63,6 +66,7 @@ _SIGNATURES = {
     "fnmt_engine_create": (_I, [C.POINTER(fnmt_arch), _I, _I, C.POINTER(_VP)]),
     "fnmt_engine_destroy": (None, [_VP]),
     "fnmt_engine_set_tensor": (_I, [_VP, C.c_char_p, _VP, _I64]),
+    "fnmt_engine_set_qtensor": (_I, [_VP, C.c_char_p, _VP, _VP, _VP, _I64, _I64]),
     "fnmt_engine_finalize": (_I, [_VP]),
     "fnmt_engine_reserve": (_I, [_VP, C.POINTER(fnmt_run)]),
     "fnmt_budgets": (_I64, [_VP, _I, _F, _I, _I, _VP]),

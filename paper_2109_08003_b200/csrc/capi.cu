@@ -95,6 +95,47 @@ int fnmt_linear(const void* A, int lda, int a_dtype, const void* W, int ldw, con
   return cuda_status(fnmt::launch_gemm(g, (cudaStream_t)stream), "fnmt_linear");
 }
 
+int64_t fnmt_qgemm_workspace(int64_t M, int K) {
+  if (M < 0 || K < 1) return fail(FNMT_E_INVALID, "fnmt_qgemm_workspace: bad arguments");
+  return fnmt::qgemm_scratch_bytes(std::max<int64_t>(M, 1), K);
+}
+
+int fnmt_qgemm(const float* A, int lda, const int8_t* Wq, const float* scale, const float* zp,
+               const int32_t* colsum, const float* bias, float* C, int ldc, int M, int N, int K,
+               int relu, void* workspace, int64_t workspace_bytes, void* stream) {
+  if (!A || !Wq || !scale || !zp || !colsum || !C || !workspace || M < 0 || N < 1 || K < 1 ||
+      lda < K || ldc < N)
+    return fail(FNMT_E_INVALID, "fnmt_qgemm: bad arguments");
+  if (M == 0) return FNMT_OK;
+  if (workspace_bytes < fnmt::qgemm_scratch_bytes(M, K))
+    return fail(FNMT_E_INVALID, "fnmt_qgemm: workspace smaller than fnmt_qgemm_workspace(M, K)");
+  const int Kp = fnmt::round_up16(K);
+  CUtensorMap tw;
+  std::string err;
+  if (!fnmt::make_tmap_8(&tw, Wq, N, Kp, 64, &err))
+    return fail(FNMT_E_INVALID, "fnmt_qgemm: " + err);
+  fnmt::GemmArgs g;
+  g.A = A;
+  g.lda = lda;
+  g.in_dtype = fnmt::kF32;
+  g.bias = bias;
+  g.M = M;
+  g.N = N;
+  g.K = K;
+  g.C = C;
+  g.ldc = ldc;
+  g.c_dtype = fnmt::kF32;
+  g.relu = relu;
+  g.qw = Wq;
+  g.qscale = scale;
+  g.qzp = zp;
+  g.qcolsum = colsum;
+  g.Kp = Kp;
+  g.qtmap_w = &tw;
+  g.qs = fnmt::qgemm_scratch(workspace, M, K);
+  return cuda_status(fnmt::launch_gemm(g, (cudaStream_t)stream), "fnmt_qgemm");
+}
+
 int fnmt_linear_argmax(const void* A, int lda, int a_dtype, const void* W, int ldw,
                        const float* bias, int M, int N, int K, uint64_t* keys_scratch,
                        int32_t* out_idx, void* stream) {
@@ -216,6 +257,16 @@ int fnmt_engine_set_tensor(fnmt_engine* e, const char* name, const float* host, 
   if (!e || !name || !host || numel < 0) return fail(FNMT_E_INVALID, "set_tensor: bad arguments");
   return guarded([&] {
     e->eng->set_tensor(name, host, numel);
+    return FNMT_OK;
+  });
+}
+
+int fnmt_engine_set_qtensor(fnmt_engine* e, const char* name, const int8_t* q, const float* scale,
+                            const float* zp, int64_t k, int64_t n) {
+  if (!e || !name || !q || !scale || !zp || k < 1 || n < 1)
+    return fail(FNMT_E_INVALID, "set_qtensor: bad arguments");
+  return guarded([&] {
+    e->eng->set_qtensor(name, q, scale, zp, k, n);
     return FNMT_OK;
   });
 }

@@ -150,6 +150,15 @@ __device__ __forceinline__ void tc_mma_f16(uint32_t tmem_d, uint64_t adesc, uint
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
+// D[tmem] (+)= A[smem] * B[smem]^T, kind::i8 (u8 / s8 in per the idesc, s32 accumulate)
+__device__ __forceinline__ void tc_mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                          uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
 // Arrive on an mbarrier once all previously issued tcgen05.mma have completed.
 __device__ __forceinline__ void tc_commit(uint64_t* bar) {
   asm volatile(
@@ -196,6 +205,40 @@ __host__ __device__ constexpr uint32_t umma_idesc_f16(int M, int N, bool bf16) {
   return (1u << 4)                                     // D format f32
          | ((bf16 ? 1u : 0u) << 7) | ((bf16 ? 1u : 0u) << 10)  // A/B format
          | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+// Instruction descriptor for kind::i8: s32 accumulate, A unsigned 8-bit
+// (quantized activations), B signed 8-bit (weights), both K-major.
+__host__ __device__ constexpr uint32_t umma_idesc_i8(int M, int N) {
+  return (2u << 4)                                     // D format s32
+         | (0u << 7) | (1u << 10)                      // A u8, B s8
+         | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+// Order-preserving 32-bit key of a float (larger float -> larger key).
+__device__ __forceinline__ unsigned int f32_key(float f) {
+  const unsigned int u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float key_f32(unsigned int k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k);
+}
+
+// Activation scale / zeropoint of quant8.quantize_activations
+// (quant8.py:171-195) from the min / max keys, in the reference's double
+// arithmetic: scale = (max - min) / 255, zp = 255 - max / scale; a constant
+// matrix takes scale 1, zp = 255 - max.
+__device__ __forceinline__ void q_act_params(const unsigned int* stats, double& scale,
+                                             double& zp) {
+  const double mx = (double)key_f32(stats[0]);
+  const double mn = (double)key_f32(~stats[1]);
+  if (mx == mn) {
+    scale = 1.0;
+    zp = __dsub_rn(255.0, mx);
+  } else {
+    scale = __ddiv_rn(__dsub_rn(mx, mn), 255.0);
+    zp = __dsub_rn(255.0, __ddiv_rn(mx, scale));
+  }
 }
 
 }  // namespace fnmt

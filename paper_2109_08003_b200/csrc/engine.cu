@@ -174,8 +174,12 @@ Engine::Engine(const fnmt_arch& a, int device, int dtype) : arch(a), device(devi
   if (a.d_model % 8 || a.ffn_dim_enc % 8 || a.ffn_dim_dec % 8)
     throw EngineError(FNMT_E_INVALID,
                       "the B200 engine needs d_model and FFN widths divisible by 8 (TMA strides)");
-  if (dtype != kF32 && dtype != kF16 && dtype != kBF16)
-    throw EngineError(FNMT_E_INVALID, "dtype must be 0 (f32), 1 (f16) or 2 (bf16)");
+  if (dtype != kF32 && dtype != kF16 && dtype != kBF16 && dtype != 3)
+    throw EngineError(FNMT_E_INVALID, "dtype must be 0 (f32), 1 (f16), 2 (bf16) or 3 (int8)");
+  if (dtype == 3) {   // int8: f32 activations everywhere, int8 GEMM weights
+    q8 = true;
+    dt = kF32;
+  }
   CK(cudaSetDevice(device));
   CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&ev_poll[0], cudaEventDisableTiming));
@@ -261,6 +265,68 @@ void Engine::set_tensor(const std::string& name, const float* host, int64_t nume
   host_tensors[name].assign(host, host + numel);
 }
 
+void Engine::set_qtensor(const std::string& name, const int8_t* q, const float* scale,
+                         const float* zp, int64_t k, int64_t n) {
+  if (!q8) throw EngineError(FNMT_E_INVALID, "set_qtensor needs an int8 engine (dtype 3)");
+  HostQ& h = host_q[name];
+  h.q.assign(q, q + k * n);
+  h.scale.assign(scale, scale + n);
+  h.zp.assign(zp, zp + n);
+  h.k = k;
+  h.n = n;
+}
+
+// int8 W^T [sum(n_i), Kp] from quantized [k, n_i] weights; the per-column
+// statistics concatenate with the columns (fused q|k|v share one activation
+// quantization because they project the same input, model.py:248-251).
+void Engine::make_qlin(Lin& L, const std::vector<std::string>& wnames, int k,
+                       const std::vector<int>& ns) {
+  const int Kp = round_up16(k);
+  int N = 0;
+  for (int n : ns) N += n;
+  std::vector<int8_t> wt((size_t)N * Kp, 0);
+  std::vector<float> sc(N), zp(N);
+  std::vector<int32_t> cs(N, 0);
+  int row0 = 0;
+  for (size_t p = 0; p < wnames.size(); ++p) {
+    auto it = host_q.find(wnames[p]);
+    if (it == host_q.end()) throw EngineError(FNMT_E_INVALID, "missing int8 tensor " + wnames[p]);
+    const HostQ& h = it->second;
+    if (h.k != k || h.n != ns[p])
+      throw EngineError(FNMT_E_INVALID, "int8 tensor " + wnames[p] + " has the wrong shape");
+    for (int i = 0; i < k; ++i)
+      for (int j = 0; j < ns[p]; ++j) {
+        const int8_t v = h.q[(size_t)i * ns[p] + j];
+        wt[(size_t)(row0 + j) * Kp + i] = v;
+        cs[row0 + j] += v;
+      }
+    std::copy(h.scale.begin(), h.scale.end(), sc.begin() + row0);
+    std::copy(h.zp.begin(), h.zp.end(), zp.begin() + row0);
+    row0 += ns[p];
+  }
+  L.Kp = Kp;
+  L.qw = (int8_t*)dalloc(wt.size());
+  CK(cudaMemcpy(L.qw, wt.data(), wt.size(), cudaMemcpyHostToDevice));
+  L.qscale = upload_f32(sc);
+  L.qzp = upload_f32(zp);
+  L.qcolsum = (int32_t*)dalloc(sizeof(int32_t) * N);
+  CK(cudaMemcpy(L.qcolsum, cs.data(), sizeof(int32_t) * N, cudaMemcpyHostToDevice));
+  std::string err;
+  if (!make_tmap_8(&L.qtm, L.qw, N, Kp, 64, &err))
+    throw EngineError(FNMT_E_CUDA, "int8 weight TMA descriptor: " + err);
+}
+
+void Engine::attach_q(GemmArgs& g, const Lin& L) const {
+  if (!L.qw) return;
+  g.qw = L.qw;
+  g.qscale = L.qscale;
+  g.qzp = L.qzp;
+  g.qcolsum = L.qcolsum;
+  g.Kp = L.Kp;
+  g.qtmap_w = &L.qtm;
+  g.qs = ws.qs;
+}
+
 const std::vector<float>& Engine::need(const std::string& name, int64_t numel) const {
   auto it = host_tensors.find(name);
   if (it == host_tensors.end()) throw EngineError(FNMT_E_INVALID, "missing tensor " + name);
@@ -300,22 +366,28 @@ Lin Engine::make_lin(const std::vector<std::string>& wnames, const std::vector<s
                      int k, const std::vector<int>& ns) {
   int N = 0;
   for (int n : ns) N += n;
-  std::vector<float> wt((size_t)N * k), bias(N);
+  std::vector<float> wt(q8 ? 0 : (size_t)N * k), bias(N);
   int row0 = 0;
   for (size_t p = 0; p < wnames.size(); ++p) {
     const int n = ns[p];
-    const auto& w = need(wnames[p], (int64_t)k * n);
     const auto& b = need(bnames[p], n);
-    for (int i = 0; i < k; ++i)
-      for (int j = 0; j < n; ++j) wt[(size_t)(row0 + j) * k + i] = w[(size_t)i * n + j];
+    if (!q8) {
+      const auto& w = need(wnames[p], (int64_t)k * n);
+      for (int i = 0; i < k; ++i)
+        for (int j = 0; j < n; ++j) wt[(size_t)(row0 + j) * k + i] = w[(size_t)i * n + j];
+    }
     std::copy(b.begin(), b.end(), bias.begin() + row0);
     row0 += n;
   }
   Lin L;
   L.N = N;
   L.K = k;
-  L.w = upload_act(wt);
   L.b = upload_f32(bias);
+  if (q8) {
+    make_qlin(L, wnames, k, ns);
+    return L;
+  }
+  L.w = upload_act(wt);
   finish_lin(L);
   return L;
 }
@@ -357,13 +429,17 @@ void Engine::finalize() {
   }
   // vocab projection W^T == out_proj table [V, d]
   {
-    const std::vector<float>* table = &src;
-    if (!arch.shared_embeddings) table = &need("out_proj", (int64_t)V * d);
     out.N = V;
     out.K = d;
-    out.w = upload_act(*table);
     out.b = upload_f32(need("out_bias", V));
-    finish_lin(out);
+    if (q8) {
+      make_qlin(out, {"out_proj"}, d, {V});   // quantized [d, vocab] projection
+    } else {
+      const std::vector<float>* table = &src;
+      if (!arch.shared_embeddings) table = &need("out_proj", (int64_t)V * d);
+      out.w = upload_act(*table);
+      finish_lin(out);
+    }
   }
   enc.clear();
   for (int i = 0; i < arch.n_enc_layers; ++i) {
@@ -401,6 +477,7 @@ void Engine::finalize() {
   }
   host_tensors.clear();
   host_tensors.rehash(0);
+  host_q.clear();
   finalized = true;
   CK(cudaDeviceSynchronize());
 }
@@ -467,6 +544,11 @@ void Engine::reserve(int tok_cap, int row_cap, int64_t pool_cap) {
   ws.out_ids = (int32_t*)alloc(sizeof(int32_t) * pool_cap);
   ws.t = (int32_t*)alloc(sizeof(int32_t) * 4);
   ws.alive = ws.t + 1;
+  if (q8) {
+    const int kmax = std::max(d, std::max(fe, fd));
+    const int64_t rows = std::max<int64_t>(tok_cap, row_cap);
+    ws.qs = qgemm_scratch(alloc(qgemm_scratch_bytes(rows, kmax)), rows, kmax);
+  }
   if (dt != kF32) {
     std::string err;
     bool ok = make_tmap_16(&ws.tm_xa, ws.xa, dt, tok_cap, d, d, 128, &err) &&
@@ -526,6 +608,7 @@ void Engine::gemm(const void* A, const CUtensorMap* tmA, int lda, const Lin& L, 
   g.relu = relu;
   g.tmap_a = tmA;
   g.tmap_w = dt == kF32 ? nullptr : &L.tm;
+  attach_q(g, L);
   const int ev = prof_begin(s);
   CK(launch_gemm(g, s));
   prof_end(s, ev, gemm_cls, 2.0 * M * L.N * L.K,
@@ -550,6 +633,7 @@ void Engine::gemm_argmax(const void* A, const CUtensorMap* tmA, int lda, int M,
   g.keys = keys;
   g.tmap_a = tmA;
   g.tmap_w = dt == kF32 ? nullptr : &out.tm;
+  attach_q(g, out);
   const int ev = prof_begin(s);
   CK(launch_gemm(g, s));
   prof_end(s, ev, FNMT_K_VOCAB, 2.0 * M * out.N * out.K,
@@ -656,6 +740,7 @@ void Engine::run_step(const StepView& v, cudaStream_t s) {
       g.t_ptr = v.t_ptr;
       g.tmap_a = tc ? &ws.tm_dxa : nullptr;
       g.tmap_w = tc ? &L.sqkv.tm : nullptr;
+      attach_q(g, L.sqkv);
       const int ev = prof_begin(s);
       CK(launch_gemm(g, s));
       prof_end(s, ev, gemm_cls, 2.0 * R * L.sqkv.N * L.sqkv.K,
@@ -927,7 +1012,7 @@ void Engine::translate_device(const int32_t* d_ids, const int64_t* d_off,
 }
 
 std::unique_ptr<Engine> Engine::make_lane() {
-  std::unique_ptr<Engine> L(new Engine(arch, device, dt));
+  std::unique_ptr<Engine> L(new Engine(arch, device, q8 ? 3 : dt));
   L->src_emb32 = src_emb32;
   L->tgt_emb32 = tgt_emb32;
   L->pos32 = pos32;
@@ -1286,6 +1371,7 @@ void Engine::cross_kv(const void* d_states_act, int rows, int layer, void* d_out
   g.ldc = 2 * arch.d_model;
   g.c_dtype = dt;
   g.tmap_w = dt == kF32 ? nullptr : &dec[layer].ckv.tm;
+  attach_q(g, dec[layer].ckv);
   CK(launch_gemm(g, stream));
   CK(cudaStreamSynchronize(stream));
 }

@@ -31,6 +31,18 @@ struct Lin {
   float* b = nullptr;  // [N]
   int N = 0, K = 0;
   CUtensorMap tm;      // TMA descriptor of W^T (tensor-core path)
+  // int8 engines: s8 W^T [N, Kp] + per-column scale / zeropoint / level sums
+  int8_t* qw = nullptr;
+  float* qscale = nullptr;
+  float* qzp = nullptr;
+  int32_t* qcolsum = nullptr;
+  int Kp = 0;
+  CUtensorMap qtm;
+};
+struct HostQ {
+  std::vector<int8_t> q;   // [k, n] row-major (reference orientation)
+  std::vector<float> scale, zp;
+  int64_t k = 0, n = 0;
 };
 struct Norm {
   float* g = nullptr;
@@ -71,6 +83,7 @@ struct Workspace {
   int32_t *t = nullptr, *alive = nullptr;
   uint8_t* finished = nullptr;
   CUtensorMap tm_xa, tm_att, tm_h, tm_dxa, tm_datt, tm_dh;
+  QScratch qs{};   // int8 engines: quantized activations of the current GEMM
   // decode attention K/V tiles (16-bit caches): self K, self V, cross K|V per layer
   std::vector<CUtensorMap> tm_sk, tm_sv, tm_ckv;
   bool kv_tma = false;
@@ -140,6 +153,9 @@ class Engine {
   ~Engine();
 
   void set_tensor(const std::string& name, const float* host, int64_t numel);
+  void set_qtensor(const std::string& name, const int8_t* q, const float* scale, const float* zp,
+                   int64_t k, int64_t n);
+  bool q8 = false;   // int8 GEMM weights (dtype code 3): activations stay f32
   void finalize();
   void reserve(int tok_cap, int row_cap, int64_t pool_cap);
   void reserve_for(const fnmt_run& run);
@@ -205,6 +221,8 @@ class Engine {
   Lin make_lin(const std::vector<std::string>& wnames, const std::vector<std::string>& bnames,
                int k, const std::vector<int>& ns);
   void finish_lin(Lin& L);
+  void make_qlin(Lin& L, const std::vector<std::string>& wnames, int k, const std::vector<int>& ns);
+  void attach_q(GemmArgs& g, const Lin& L) const;
   Norm make_norm(const std::string& prefix);
   float emb_scale() const;
 
@@ -230,6 +248,7 @@ class Engine {
   void ensure_meta(size_t rows, size_t cus);
 
   std::unordered_map<std::string, std::vector<float>> host_tensors;
+  std::unordered_map<std::string, HostQ> host_q;
   bool finalized = false;
   std::vector<void*> allocations;
   float* src_emb32 = nullptr;

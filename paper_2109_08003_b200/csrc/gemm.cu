@@ -55,6 +55,14 @@ struct EpiParams {
   void* vc;
   int cap, seg;
   const int32_t* t_ptr;
+  // int8 path: per-column weight scale / zeropoint / column sums, per-row
+  // activation sums, activation min / max keys, real (unpadded) K
+  const float* qscale;
+  const float* qzp;
+  const int32_t* qcolsum;
+  const int32_t* rowsum;
+  const unsigned int* stats;
+  int qk;
 };
 
 // kEpiQKV destination of output element (m, n): q columns go to C, k / v
@@ -225,15 +233,43 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& ep, int m, int n
   }
 }
 
+// int8 epilogue: turn 32 s32 accumulators of row m into the f32 value of
+// quant8.qgemm (quant8.py:246-278) — the zeropoint cross terms expanded
+// against the row / column sums, evaluated in double in the reference's
+// operation order with explicit round-to-nearest ops (no FMA contraction),
+// then rounded once to f32:
+//   corr = ((acc - bzp*rowsum) - azp*colsum) + (K*azp)*bzp
+//   out  = f32((ascale*bscale) * corr)
+__device__ __forceinline__ void q_dequant_chunk(const EpiParams& ep, int m, float (&v)[32],
+                                                const float* sc, const float* zp,
+                                                const int32_t* cs) {
+  double ascale, azp;
+  q_act_params(ep.stats, ascale, azp);
+  const double kazp = __dmul_rn((double)ep.qk, azp);
+  const double rs = (double)ep.rowsum[m];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const double acc = (double)__float_as_int(v[i]);
+    const double bz = (double)zp[i];
+    double t = __dsub_rn(acc, __dmul_rn(bz, rs));
+    t = __dsub_rn(t, __dmul_rn(azp, (double)cs[i]));
+    t = __dadd_rn(t, __dmul_rn(kazp, bz));
+    v[i] = __double2float_rn(__dmul_rn(__dmul_rn(ascale, (double)sc[i]), t));
+  }
+}
+
 // ---------------------------------------------------------------------------
 // persistent tcgen05 kernel
 
-template <int BN, int STAGES>
+// Every stage row is 128 bytes of K: 64 fp16/bf16 elements, or 128 int8.
+template <int BN, int STAGES, bool I8 = false>
 struct TcCfg {
+  static constexpr int kBKe = I8 ? 2 * kBK : kBK;   // K elements per stage
   static constexpr int kBBytes = BN * kBK * 2;
   static constexpr int kStage = kABytes + kBBytes;
   static constexpr int kTmemCols = 2 * BN;   // double-buffered accumulator
-  static constexpr int kSmem = 1024 + STAGES * kStage + 2 * BN * 4 + 256;
+  static constexpr int kColBytes = I8 ? 16 : 4;   // bias (+ scale, zeropoint, column sum)
+  static constexpr int kSmem = 1024 + STAGES * kStage + 2 * BN * kColBytes + 256;
 };
 
 constexpr int kEpiWarps = 8;                       // 2 per TMEM lane quarter
@@ -309,18 +345,22 @@ __device__ __forceinline__ void topk_epilogue(const EpiParams& ep, uint32_t tadd
   }
 }
 
-template <int BN, int STAGES, int TOPK>
+template <int BN, int STAGES, int TOPK, bool I8 = false>
 __global__ void __launch_bounds__(kTcThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmw,
                    int K, uint32_t idesc, EpiParams ep, int tiles_n, int tiles) {
-  using Cfg = TcCfg<BN, STAGES>;
+  using Cfg = TcCfg<BN, STAGES, I8>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
   uint8_t* sA = base;
   uint8_t* sB = base + STAGES * kABytes;
   float* bias_s = reinterpret_cast<float*>(sB + STAGES * Cfg::kBBytes);   // [2][BN]
-  uint64_t* full = reinterpret_cast<uint64_t*>(bias_s + 2 * BN);
+  // int8: [2][BN] column scale, zeropoint, column sum after the bias
+  float* qsc_s = bias_s + 2 * BN;
+  float* qzp_s = qsc_s + (I8 ? 2 * BN : 0);
+  int32_t* qcs_s = reinterpret_cast<int32_t*>(qzp_s + (I8 ? 2 * BN : 0));
+  uint64_t* full = reinterpret_cast<uint64_t*>(bias_s + (Cfg::kColBytes / 4) * 2 * BN);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
@@ -328,7 +368,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int nk = (K + kBK - 1) / kBK;
+  const int nk = (K + Cfg::kBKe - 1) / Cfg::kBKe;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tma);
@@ -363,10 +403,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(empty + s, ph ^ 1);
           mbar_expect_tx(full + s, Cfg::kStage);
-          tma_load_2d(sA + s * kABytes, &tma, full + s, kb * kBK, m0);
+          tma_load_2d(sA + s * kABytes, &tma, full + s, kb * Cfg::kBKe, m0);
 #pragma unroll
           for (int j = 0; j < BN / kWBox; ++j)
-            tma_load_2d(sB + s * Cfg::kBBytes + j * kWBox * 128, &tmw, full + s, kb * kBK,
+            tma_load_2d(sB + s * Cfg::kBBytes + j * kWBox * 128, &tmw, full + s, kb * Cfg::kBKe,
                         n0 + j * kWBox);
           if (++s == STAGES) {
             s = 0;
@@ -390,9 +430,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           tc_fence_after();
           const uint64_t ad = umma_desc_sw128(smem_u32(sA + s * kABytes));
           const uint64_t bd = umma_desc_sw128(smem_u32(sB + s * Cfg::kBBytes));
+          // 4 MMAs of 32 bytes of K each (K = 16 fp16 or K = 32 int8)
 #pragma unroll
-          for (int kk = 0; kk < kBK / 16; ++kk)
-            tc_mma_f16(d, ad + 2 * kk, bd + 2 * kk, idesc, (kb | kk) != 0 ? 1u : 0u);
+          for (int kk = 0; kk < 4; ++kk) {
+            if constexpr (I8)
+              tc_mma_i8(d, ad + 2 * kk, bd + 2 * kk, idesc, (kb | kk) != 0 ? 1u : 0u);
+            else
+              tc_mma_f16(d, ad + 2 * kk, bd + 2 * kk, idesc, (kb | kk) != 0 ? 1u : 0u);
+          }
           tc_commit(empty + s);
           if (++s == STAGES) {
             s = 0;
@@ -416,8 +461,15 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       const int n0 = (tile % tiles_n) * BN;
       // stage this tile's bias while the MMAs run (double-buffered by acc)
       float* bs = bias_s + acc * BN;
-      for (int i = threadIdx.x - 64; i < BN; i += kEpiWarps * 32)
-        bs[i] = (ep.bias && n0 + i < ep.N) ? ep.bias[n0 + i] : 0.f;
+      for (int i = threadIdx.x - 64; i < BN; i += kEpiWarps * 32) {
+        const bool in = n0 + i < ep.N;
+        bs[i] = (ep.bias && in) ? ep.bias[n0 + i] : 0.f;
+        if constexpr (I8) {
+          qsc_s[acc * BN + i] = in ? ep.qscale[n0 + i] : 0.f;
+          qzp_s[acc * BN + i] = in ? ep.qzp[n0 + i] : 0.f;
+          qcs_s[acc * BN + i] = in ? ep.qcolsum[n0 + i] : 0;
+        }
+      }
       named_bar_sync(1, kEpiWarps * 32);
       mbar_wait(tfull + acc, aph);
       tc_fence_after();
@@ -438,6 +490,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           float v[32];
           tmem_ld32(taddr + c * 32, v);
           const int nb = n0 + col0 + c * 32;
+          if constexpr (I8) {
+            if (row_ok && nb < ep.N) {
+              const int o = acc * BN + col0 + c * 32;
+              q_dequant_chunk(ep, m, v, qsc_s + o, qzp_s + o, qcs_s + o);
+            }
+          }
           if (row_ok && nb < ep.N)
             epilogue_chunk(ep, m, nb, v, bs + col0 + c * 32, best_v, best_i);
         }
@@ -539,19 +597,19 @@ int num_sms() {
   return n;
 }
 
-template <int BN, int STAGES, int TOPK = 0>
+template <int BN, int STAGES, int TOPK = 0, bool I8 = false>
 cudaError_t launch_tc(const CUtensorMap& ta, const CUtensorMap& tw, const GemmArgs& g,
                       const EpiParams& ep, cudaStream_t s) {
-  using Cfg = TcCfg<BN, STAGES>;
+  using Cfg = TcCfg<BN, STAGES, I8>;
   static_assert(Cfg::kSmem <= 227 * 1024, "GEMM stage ring exceeds shared memory");
-  cudaError_t e = set_max_smem((const void*)gemm_tc_kernel<BN, STAGES, TOPK>);
+  cudaError_t e = set_max_smem((const void*)gemm_tc_kernel<BN, STAGES, TOPK, I8>);
   if (e != cudaSuccess) return e;
   const int tiles_n = (g.N + BN - 1) / BN;
   const int tiles = tiles_n * ((g.M + kBM - 1) / kBM);
   const int grid = tiles < num_sms() ? tiles : num_sms();
-  const uint32_t idesc = umma_idesc_f16(kBM, BN, g.in_dtype == kBF16);
-  return launch_k(gemm_tc_kernel<BN, STAGES, TOPK>, dim3(grid), dim3(kTcThreads),
-                  (size_t)Cfg::kSmem, s, ta, tw, g.K, idesc, ep, tiles_n, tiles);
+  const uint32_t idesc = I8 ? umma_idesc_i8(kBM, BN) : umma_idesc_f16(kBM, BN, g.in_dtype == kBF16);
+  return launch_k(gemm_tc_kernel<BN, STAGES, TOPK, I8>, dim3(grid), dim3(kTcThreads),
+                  (size_t)Cfg::kSmem, s, ta, tw, I8 ? g.Kp : g.K, idesc, ep, tiles_n, tiles);
 }
 
 }  // namespace
@@ -633,8 +691,10 @@ int pick_bn(int M, int N) {
 
 cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t s) {
   if (g.M <= 0 || g.N <= 0) return cudaSuccess;
+  if (g.qw) return launch_qgemm(g, s);
   EpiParams ep{g.bias, g.M, g.N, g.epi, g.C, g.ldc, g.c_dtype, g.relu, g.resid, g.ld_resid,
-               g.keys, g.topk, g.kc, g.vc, g.cap, g.seg, g.t_ptr};
+               g.keys, g.topk, g.kc, g.vc, g.cap, g.seg, g.t_ptr,
+               nullptr, nullptr, nullptr, nullptr, nullptr, 0};
   if (g.epi == kEpiQKV && (!g.kc || !g.vc || !g.t_ptr || g.seg <= 0 || g.N != 3 * g.seg))
     return cudaErrorInvalidValue;
   if (g.epi == kEpiTopK && (g.in_dtype == kF32 || (g.topk.K != 4 && g.topk.K != 8)))
@@ -668,6 +728,44 @@ cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t s) {
     case 128: return launch_tc<128, 6>(*pa, *pw, g, ep, s);
     default: return launch_tc<64, 8>(*pa, *pw, g, ep, s);
   }
+}
+
+// int8 tcgen05 GEMM over activations already quantized into g.qs (qgemm.cu).
+cudaError_t launch_tc_i8(const CUtensorMap& ta, const GemmArgs& g, cudaStream_t s) {
+  if (g.epi == kEpiTopK || !g.qtmap_w) return cudaErrorInvalidValue;
+  EpiParams ep{g.bias, g.M, g.N, g.epi, g.C, g.ldc, g.c_dtype, g.relu, g.resid, g.ld_resid,
+               g.keys, g.topk, g.kc, g.vc, g.cap, g.seg, g.t_ptr,
+               g.qscale, g.qzp, g.qcolsum, g.qs.rowsum, g.qs.stats, g.K};
+  switch (pick_bn(g.M, g.N)) {
+    case 256: return launch_tc<256, 4, 0, true>(ta, *g.qtmap_w, g, ep, s);
+    case 128: return launch_tc<128, 6, 0, true>(ta, *g.qtmap_w, g, ep, s);
+    default: return launch_tc<64, 8, 0, true>(ta, *g.qtmap_w, g, ep, s);
+  }
+}
+
+bool make_tmap_8(CUtensorMap* out, const void* base, int64_t rows, int64_t kp, int box_rows,
+                 std::string* err) {
+  auto fn = encode_fn();
+  if (!fn) {
+    if (err) *err = "cuTensorMapEncodeTiled unavailable (driver too old?)";
+    return false;
+  }
+  if ((reinterpret_cast<uintptr_t>(base) & 15) || (kp & 15)) {
+    if (err) *err = "int8 TMA operand must be 16-byte aligned with K padded to 16";
+    return false;
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)kp, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)kp};
+  cuuint32_t box[2] = {128u, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(out, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    if (err) *err = "cuTensorMapEncodeTiled (int8) failed with CUresult " + std::to_string((int)r);
+    return false;
+  }
+  return true;
 }
 
 }  // namespace fnmt

@@ -66,6 +66,24 @@ struct TopKPartials {
   int K;           // 4 or 8 entries kept per tile
 };
 
+// Per-call scratch of the int8 GEMM: quantized activations [M, Kp] u8,
+// their row sums, and the min / max keys of the f32 input.
+struct QScratch {
+  uint8_t* qa = nullptr;
+  int32_t* rowsum = nullptr;
+  unsigned int* stats = nullptr;   // [0] = key(max), [1] = ~key(min)  (zeroed per call)
+  int64_t qa_bytes = 0;
+  int64_t rows = 0;
+};
+inline int round_up16(int k) { return (k + 15) & ~15; }
+int64_t qgemm_scratch_bytes(int64_t M, int K);   // qa + rowsum + stats, 256-B aligned parts
+QScratch qgemm_scratch(void* base, int64_t M, int K);
+
+// Encode the TMA descriptor of an s8 / u8 row-major [rows, Kp] matrix (box
+// = [box_rows, 128 bytes], 128-B swizzle) for the int8 tcgen05 GEMM.
+bool make_tmap_8(CUtensorMap* out, const void* base, int64_t rows, int64_t kp, int box_rows,
+                 std::string* err);
+
 struct GemmArgs {
   const void* A = nullptr;  // [M, K] row-major, leading dim lda (elements)
   int lda = 0;
@@ -91,6 +109,17 @@ struct GemmArgs {
   // them on the fly (host cost ~ microseconds).
   const CUtensorMap* tmap_a = nullptr;
   const CUtensorMap* tmap_w = nullptr;
+  // int8 path (quant8.py): A is f32 [M, K] activations, quantized per call to
+  // u8 with one scale / zeropoint over the whole matrix; W is s8 W^T [N, Kp]
+  // (Kp = K rounded up to 16, zero padded) with per-column scale / zeropoint
+  // and column sums.  Set qw to select it (in_dtype must be kF32).
+  const int8_t* qw = nullptr;
+  const float* qscale = nullptr;
+  const float* qzp = nullptr;
+  const int32_t* qcolsum = nullptr;
+  int Kp = 0;
+  const CUtensorMap* qtmap_w = nullptr;
+  QScratch qs{};
 };
 
 // Encode a 2-D TMA descriptor for a row-major [rows, cols] 16-bit matrix with
@@ -101,6 +130,9 @@ bool make_tmap_16(CUtensorMap* out, const void* base, int dtype, int64_t rows, i
 int gemm_tile_n();  // N tile of the tcgen05 kernel (for W descriptors)
 
 cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t s);
+// int8: quantize A (min / max, u8 + row sums) then the s8 tcgen05 GEMM (qgemm.cu)
+cudaError_t launch_qgemm(const GemmArgs& g, cudaStream_t s);
+cudaError_t launch_tc_i8(const CUtensorMap& ta, const GemmArgs& g, cudaStream_t s);
 
 // ---------------------------------------------------------------------------
 // row kernels

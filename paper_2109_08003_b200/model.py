@@ -27,8 +27,10 @@ import torch
 from . import _capi
 from ._capi import check, lib, ptr
 from .store import ModelConfig, config_of, iter_named_tensors
+from .quant8 import iter_float_tensors, iter_quantized
 
-_TORCH_DT = {_capi.F32: torch.float32, _capi.F16: torch.float16, _capi.BF16: torch.bfloat16}
+_TORCH_DT = {_capi.F32: torch.float32, _capi.F16: torch.float16, _capi.BF16: torch.bfloat16,
+             _capi.INT8: torch.float32}   # int8 engines keep f32 activations
 
 
 class LengthError(ValueError):
@@ -56,11 +58,31 @@ class EngineHandle:
         check(lib.fnmt_engine_create(C.byref(arch), device, self.dtype, C.byref(h)),
               "fnmt_engine_create")
         self.h = h
-        for name, arr in iter_named_tensors(self.cfg, weights):
+        if self.dtype == _capi.INT8:
+            self._upload_int8(weights)
+        else:
+            for name, arr in iter_named_tensors(self.cfg, weights):
+                arr = np.ascontiguousarray(arr, dtype=np.float32)
+                check(lib.fnmt_engine_set_tensor(self.h, name.encode(), arr.ctypes.data,
+                                                 arr.size), f"set_tensor({name})")
+        check(lib.fnmt_engine_finalize(self.h), "finalize")
+
+    def _upload_int8(self, weights):
+        """int8 precision (store.py:29-36): every GEMM weight (and the output
+        projection, [d, vocab]) goes up as s8 + per-column scale / zeropoint;
+        f32 weights are quantized here, once, like the reference's
+        quantize-at-load (store.py:490-524)."""
+        for name, arr in iter_float_tensors(self.cfg, weights):
             arr = np.ascontiguousarray(arr, dtype=np.float32)
             check(lib.fnmt_engine_set_tensor(self.h, name.encode(), arr.ctypes.data, arr.size),
                   f"set_tensor({name})")
-        check(lib.fnmt_engine_finalize(self.h), "finalize")
+        for name, qm in iter_quantized(self.cfg, weights):
+            q = np.ascontiguousarray(qm.q, dtype=np.int8)
+            sc = np.ascontiguousarray(qm.col_scale, dtype=np.float32)
+            zp = np.ascontiguousarray(qm.col_zeropoint, dtype=np.float32)
+            check(lib.fnmt_engine_set_qtensor(self.h, name.encode(), q.ctypes.data,
+                                              sc.ctypes.data, zp.ctypes.data, q.shape[0],
+                                              q.shape[1]), f"set_qtensor({name})")
 
     @property
     def torch_dtype(self):

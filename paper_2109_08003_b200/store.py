@@ -220,20 +220,25 @@ def random_model(cfg: ModelConfig, seed: int) -> Weights:
     return _assemble(cfg, arrays)
 
 
-def iter_named_tensors(cfg: ModelConfig, w) -> Iterator[tuple[str, np.ndarray]]:
+def iter_named_tensors(cfg: ModelConfig, w, skip_gemm: bool = False
+                       ) -> Iterator[tuple[str, np.ndarray]]:
     """(manifest name, float32 array) pairs of a Weights-like object, in the
     reference orientation (gemm weights [k, n]; out_proj as its [vocab, d]
-    table).  Works for the reference's Weights too (duck-typed)."""
+    table).  Works for the reference's Weights too (duck-typed).  With
+    ``skip_gemm`` the GEMM weights (and an unshared out_proj) are left out —
+    the int8 upload sends those quantized (quant8.iter_quantized)."""
     yield "src_embed", np.asarray(w.src_embed, np.float32)
     if not cfg.shared_embeddings:
         yield "tgt_embed", np.asarray(w.tgt_embed, np.float32)
-        yield "out_proj", np.asarray(w.out_proj.weight, np.float32).T
+        if not skip_gemm:
+            yield "out_proj", np.asarray(w.out_proj.weight, np.float32).T
     yield "out_bias", np.asarray(w.out_proj.bias, np.float32)
 
     def block(prefix, blk):
         for part in "qkvo":
             pr = getattr(blk, part)
-            yield f"{prefix}.{part}_w", np.asarray(pr.weight, np.float32)
+            if not skip_gemm:
+                yield f"{prefix}.{part}_w", np.asarray(pr.weight, np.float32)
             yield f"{prefix}.{part}_b", np.asarray(pr.bias, np.float32)
 
     def norm(prefix, n):
@@ -241,10 +246,10 @@ def iter_named_tensors(cfg: ModelConfig, w) -> Iterator[tuple[str, np.ndarray]]:
         yield f"{prefix}.bias", np.asarray(n.bias, np.float32)
 
     def ffn(prefix, f):
-        yield f"{prefix}.w1", np.asarray(f.w1.weight, np.float32)
-        yield f"{prefix}.b1", np.asarray(f.w1.bias, np.float32)
-        yield f"{prefix}.w2", np.asarray(f.w2.weight, np.float32)
-        yield f"{prefix}.b2", np.asarray(f.w2.bias, np.float32)
+        for wn, bn, pr in (("w1", "b1", f.w1), ("w2", "b2", f.w2)):
+            if not skip_gemm:
+                yield f"{prefix}.{wn}", np.asarray(pr.weight, np.float32)
+            yield f"{prefix}.{bn}", np.asarray(pr.bias, np.float32)
 
     for i, L in enumerate(w.enc_layers):
         yield from block(f"enc.{i}.attn", L.attn)

@@ -639,6 +639,7 @@ cudaError_t decode_dispatch(const DecAttnArgs& a, cudaStream_t s) {
 
 cudaError_t launch_attention_varlen(const AttnArgs& a, cudaStream_t s) {
   if (a.n_seq <= 0 || a.max_q <= 0) return cudaSuccess;
+  if (attention_mma_ok(a)) return launch_attention_varlen_mma(a, s);
   switch (a.dtype) {
     case kF32: return varlen_dispatch<float>(a, s);
     case kF16: return varlen_dispatch<__half>(a, s);

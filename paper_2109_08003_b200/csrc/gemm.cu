@@ -345,8 +345,8 @@ __device__ __forceinline__ void topk_epilogue(const EpiParams& ep, uint32_t tadd
   }
 }
 
-template <int BN, int STAGES, int TOPK, bool I8 = false>
-__global__ void __launch_bounds__(kTcThreads, 1)
+template <int BN, int STAGES, int TOPK, bool I8 = false, int MINB = 1>
+__global__ void __launch_bounds__(kTcThreads, MINB)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmw,
                    int K, uint32_t idesc, EpiParams ep, int tiles_n, int tiles) {
   using Cfg = TcCfg<BN, STAGES, I8>;
@@ -597,24 +597,37 @@ int num_sms() {
   return n;
 }
 
-template <int BN, int STAGES, int TOPK = 0, bool I8 = false>
+// MINB = 2: two co-resident CTAs per SM (half-depth stage ring, <= 96
+// registers) for the skinny decoder GEMMs, so a second tile (or another
+// decode lane's kernel) hides the TMA / MMA / epilogue latency of the first.
+template <int BN, int STAGES, int TOPK = 0, bool I8 = false, int MINB = 1>
 cudaError_t launch_tc(const CUtensorMap& ta, const CUtensorMap& tw, const GemmArgs& g,
                       const EpiParams& ep, cudaStream_t s) {
   using Cfg = TcCfg<BN, STAGES, I8>;
   static_assert(Cfg::kSmem <= 227 * 1024, "GEMM stage ring exceeds shared memory");
-  cudaError_t e = set_max_smem((const void*)gemm_tc_kernel<BN, STAGES, TOPK, I8>);
+  static_assert(MINB == 1 || MINB * (Cfg::kSmem + 1024) <= 228 * 1024, "MINB CTAs do not fit");
+  cudaError_t e = set_max_smem((const void*)gemm_tc_kernel<BN, STAGES, TOPK, I8, MINB>);
   if (e != cudaSuccess) return e;
   const int tiles_n = (g.N + BN - 1) / BN;
   const int tiles = tiles_n * ((g.M + kBM - 1) / kBM);
-  const int grid = tiles < num_sms() ? tiles : num_sms();
+  const int grid = tiles < MINB * num_sms() ? tiles : MINB * num_sms();
   const uint32_t idesc = I8 ? umma_idesc_i8(kBM, BN) : umma_idesc_f16(kBM, BN, g.in_dtype == kBF16);
-  return launch_k(gemm_tc_kernel<BN, STAGES, TOPK, I8>, dim3(grid), dim3(kTcThreads),
+  return launch_k(gemm_tc_kernel<BN, STAGES, TOPK, I8, MINB>, dim3(grid), dim3(kTcThreads),
                   (size_t)Cfg::kSmem, s, ta, tw, I8 ? g.Kp : g.K, idesc, ep, tiles_n, tiles);
 }
 
 }  // namespace
 
 int gemm_tile_n() { return kWBox; }
+
+bool dual_cta_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("FNMT_GEMM_DUAL");
+    on = !(e && e[0] == '0');
+  }
+  return on != 0;
+}
 
 bool pdl_enabled() {
   static int on = -1;
@@ -726,7 +739,9 @@ cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t s) {
   switch (pick_bn(g.M, g.N)) {
     case 256: return launch_tc<256, 4>(*pa, *pw, g, ep, s);
     case 128: return launch_tc<128, 6>(*pa, *pw, g, ep, s);
-    default: return launch_tc<64, 8>(*pa, *pw, g, ep, s);
+    default:
+      if (g.K <= 1024 && dual_cta_enabled()) return launch_tc<64, 4, 0, false, 2>(*pa, *pw, g, ep, s);
+      return launch_tc<64, 8>(*pa, *pw, g, ep, s);
   }
 }
 

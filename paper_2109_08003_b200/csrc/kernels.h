@@ -30,6 +30,7 @@ inline cudaError_t set_max_smem(const void* func) {
 // FNMT_PDL=0.  Kernels launched this way call pdl_wait() before touching
 // their predecessor's data (common.cuh).
 bool pdl_enabled();
+bool dual_cta_enabled();   // FNMT_GEMM_DUAL=0 disables 2-CTA/SM decoder GEMMs
 template <typename... KArgs, typename... Args>
 cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                      Args&&... args) {
@@ -166,6 +167,9 @@ struct AttnArgs {
   int n_seq, max_q, max_k;
 };
 cudaError_t launch_attention_varlen(const AttnArgs& a, cudaStream_t s);
+// tensor-core (mma.sync) variant for fp16 / bf16, dk % 16 == 0, <= 256 keys (attn_mma.cu)
+bool attention_mma_ok(const AttnArgs& a);
+cudaError_t launch_attention_varlen_mma(const AttnArgs& a, cudaStream_t s);
 
 // Single-query attention for the incremental decoder.
 // Self mode: keys of row r live at kv + (r*cap + j)*ldkv, j in [0, len) where

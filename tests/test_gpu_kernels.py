@@ -193,3 +193,29 @@ def test_attention_all_masked_row_follows_reference():
           "attention")
     torch.cuda.synchronize()
     assert np.abs(out.cpu().numpy().reshape(b, s, d) - want).max() <= 1e-5
+
+
+@pytest.mark.parametrize("heads,d,lens", [(1, 512, [7, 1, 23, 40]), (8, 512, [24, 3, 65, 17]),
+                                          (8, 768, [9, 31]), (2, 64, [200, 130, 5]),
+                                          (1, 64, [300, 12]), (4, 64, [0, 6])])
+def test_varlen_attention_f16_tensor_core(heads, d, lens):
+    """fp16 storage: the mma.sync encoder attention (<= 256 keys) and the SIMT
+    fallback (longer) against the fp32 oracle on fp16-rounded inputs; a
+    zero-length key set exercises the all-masked -1e9 rule."""
+    rng = np.random.default_rng(heads * 1000 + d + len(lens))
+    b, s = len(lens), max(max(lens), 1)
+    q, k, v = (rng.standard_normal((b, s, d)).astype(np.float16).astype(np.float32)
+               for _ in range(3))
+    valid = np.arange(s)[None, :] < np.array(lens)[:, None]
+    want = O.mha(q, k, v, O.key_mask(valid), heads)
+    Q, K_, V_ = (torch.from_numpy(a.reshape(b * s, d)).half().to(DEV) for a in (q, k, v))
+    out = torch.zeros((b * s, d), device=DEV, dtype=torch.float16)
+    start = torch.arange(b, dtype=torch.int32, device=DEV) * s
+    qlen = torch.full((b,), s, dtype=torch.int32, device=DEV)
+    klen = torch.tensor(lens, dtype=torch.int32, device=DEV)
+    check(lib.fnmt_attention(ptr(Q), d, ptr(K_), ptr(V_), d, ptr(out), d, _capi.F16, heads,
+                             d // heads, ptr(start), ptr(qlen), ptr(start), ptr(klen), s, b, s, s,
+                             stream()), "attention")
+    torch.cuda.synchronize()
+    got = out.float().cpu().numpy().reshape(b, s, d)
+    assert np.abs(got - want).max() <= 1e-2 * max(1.0, np.abs(want).max())

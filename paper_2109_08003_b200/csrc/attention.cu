@@ -269,7 +269,7 @@ __device__ __forceinline__ void softmax_inplace(float* S, int nk) {
 // G lanes cooperate on one key (CH 16-byte chunks each); 32/G keys per warp.
 // NT threads per (row, head): 128 normally, 512 when there are too few rows
 // to fill the machine (long-sentence batches).
-template <typename T, int G, int CH, int NT>
+template <typename T, int G, int CH, int NT, int U = 1>
 __global__ void __launch_bounds__(NT) attn_decode_kernel(DecAttnArgs a, float qscale) {
   pdl_trigger();
   pdl_wait();
@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(NT) attn_decode_kernel(DecAttnArgs a, float qs
 
   const T* kb = reinterpret_cast<const T*>(a.k) + h * dk;
   constexpr int KPW = 32 / G;            // keys per warp per round (lane groups)
-  constexpr int U = 1;                   // rounds unrolled: U * KPW keys in flight per warp
+  // U rounds unrolled: U * KPW keys (U * CH 16-byte loads per lane) in flight per warp
   const int g = lane / G, li = lane % G;
   const int stride = (NT / 32) * KPW;
   for (int j0 = warp * KPW; j0 < c.nk; j0 += stride * U) {
@@ -337,7 +337,7 @@ __global__ void __launch_bounds__(NT) attn_decode_kernel(DecAttnArgs a, float qs
 #pragma unroll
   for (int i = 0; i < VEC; ++i) acc[i] = 0.f;
   if (grp < groups) {
-    constexpr int U3 = 1;   // value rows in flight per thread
+    constexpr int U3 = U;   // value rows in flight per thread
     for (int j0 = grp; j0 < c.nk; j0 += groups * U3) {
       float f[U3][VEC];
       float w[U3];
@@ -567,17 +567,36 @@ cudaError_t varlen_dispatch(const AttnArgs& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-template <typename T, int G, int CH, int NT>
-cudaError_t launch_dec_nt(const DecAttnArgs& a, float qscale, cudaStream_t s) {
+int dec_unroll() {
+  static int u = -1;
+  if (u < 0) {
+    const char* e = getenv("FNMT_DEC_U");
+    u = e ? atoi(e) : 1;
+    if (u != 2 && u != 4) u = 1;
+  }
+  return u;
+}
+
+template <typename T, int G, int CH, int NT, int U>
+cudaError_t launch_dec_nt_u(const DecAttnArgs& a, float qscale, cudaStream_t s) {
   const int groups = NT / (a.dk / Vec16<T>::N);
   const size_t smem = sizeof(float) * ((size_t)a.dk + a.max_k + 4 + (size_t)groups * a.dk);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
   if (smem > 48 * 1024) {
-    cudaError_t e = set_max_smem((const void*)attn_decode_kernel<T, G, CH, NT>);
+    cudaError_t e = set_max_smem((const void*)attn_decode_kernel<T, G, CH, NT, U>);
     if (e != cudaSuccess) return e;
   }
-  return launch_k(attn_decode_kernel<T, G, CH, NT>, dim3(a.rows, a.heads), dim3(NT), smem, s, a,
+  return launch_k(attn_decode_kernel<T, G, CH, NT, U>, dim3(a.rows, a.heads), dim3(NT), smem, s, a,
                   qscale);
+}
+
+template <typename T, int G, int CH, int NT>
+cudaError_t launch_dec_nt(const DecAttnArgs& a, float qscale, cudaStream_t s) {
+  switch (dec_unroll()) {
+    case 4: return launch_dec_nt_u<T, G, CH, NT, 4>(a, qscale, s);
+    case 2: return launch_dec_nt_u<T, G, CH, NT, 2>(a, qscale, s);
+    default: return launch_dec_nt_u<T, G, CH, NT, 1>(a, qscale, s);
+  }
 }
 
 template <typename T, int G, int CH, int NT>

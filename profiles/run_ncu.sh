@@ -5,7 +5,7 @@
 #      one decode lane so the launch order is phase-ordered);
 #   2. --set full captures of the decode GEMM, vocab GEMM, decode attention,
 #      encoder attention and add+LayerNorm kernels, exported as raw CSV.
-# Output under gpurun_out/ (gzipped; the .ncu-rep files are kept if small).
+# Output under gpurun_out/ (raw-page CSVs gzipped; the .ncu-rep files are dropped).
 set -u
 R=${1:-r1}
 mkdir -p gpurun_out
@@ -14,9 +14,10 @@ ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,
     --clock-control none --csv --log-file gpurun_out/launches_$R.csv \
     python -m paper_2109_08003_b200.profile_step 2048 > gpurun_out/ncu_launches_$R.log 2>&1
 gzip -f gpurun_out/launches_$R.csv
-for spec in "gemm_dec:regex:gemm_tc_kernel<64:400:3" "vocab:regex:gemm_tc_kernel<256:40:2" \
-            "attn_dec:regex:attn_decode:200:2" "attn_enc:regex:attn_varlen:4:1" \
-            "norm:regex:add_norm:300:2"; do
+# ncu -k matches the base kernel name (no template arguments): 7 consecutive
+# GEMMs from launch 100 on are one full decode step (6 decoder GEMMs + vocab).
+for spec in "gemm_step:regex:gemm_tc:100:7" "attn_dec:regex:attn_decode:200:2" \
+            "attn_enc:regex:attn_varlen:4:1" "norm:regex:add_norm:300:2"; do
   IFS=: read name kind pat skip cnt <<< "$spec"
   ncu --set full --clock-control none --import-source on -k "$kind:$pat" --launch-skip $skip \
       --launch-count $cnt -o gpurun_out/full_${R}_$name \
@@ -24,6 +25,6 @@ for spec in "gemm_dec:regex:gemm_tc_kernel<64:400:3" "vocab:regex:gemm_tc_kernel
   ncu -i gpurun_out/full_${R}_$name.ncu-rep --page raw --csv > gpurun_out/full_${R}_$name.csv 2>/dev/null
   gzip -f gpurun_out/full_${R}_$name.csv
   sz=$(stat -c %s gpurun_out/full_${R}_$name.ncu-rep 2>/dev/null || echo 0)
-  if [ "$sz" -gt 12000000 ]; then rm -f gpurun_out/full_${R}_$name.ncu-rep; fi
+  if [ "$sz" -gt 0 ]; then rm -f gpurun_out/full_${R}_$name.ncu-rep; fi
 done
 ls -la gpurun_out

@@ -269,7 +269,39 @@ __device__ __forceinline__ void softmax_inplace(float* S, int nk) {
 // G lanes cooperate on one key (CH 16-byte chunks each); 32/G keys per warp.
 // NT threads per (row, head): 128 normally, 512 when there are too few rows
 // to fill the machine (long-sentence batches).
-template <typename T, int G, int CH, int NT, int U = 1>
+template <typename T>
+__device__ __forceinline__ void cvt16(const uint4& u, float (&f)[Vec16<T>::N]);
+template <>
+__device__ __forceinline__ void cvt16<float>(const uint4& u, float (&f)[4]) {
+  f[0] = __uint_as_float(u.x); f[1] = __uint_as_float(u.y);
+  f[2] = __uint_as_float(u.z); f[3] = __uint_as_float(u.w);
+}
+template <>
+__device__ __forceinline__ void cvt16<__half>(const uint4& u, float (&f)[8]) {
+  const __half2* h = reinterpret_cast<const __half2*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 x = __half22float2(h[i]);
+    f[2 * i] = x.x;
+    f[2 * i + 1] = x.y;
+  }
+}
+template <>
+__device__ __forceinline__ void cvt16<__nv_bfloat16>(const uint4& u, float (&f)[8]) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 x = __bfloat1622float2(h[i]);
+    f[2 * i] = x.x;
+    f[2 * i + 1] = x.y;
+  }
+}
+
+// U: score rounds in flight per warp (U * KPW keys, U * CH raw 16-byte
+// vectors per lane); UV: value rows in flight per thread.  Loads land in raw
+// uint4 registers and are widened to fp32 only at the FMA, so deeper unrolls
+// cost 4 registers per vector instead of 8 floats.
+template <typename T, int G, int CH, int NT, int U = 1, int UV = 1>
 __global__ void __launch_bounds__(NT) attn_decode_kernel(DecAttnArgs a, float qscale) {
   pdl_trigger();
   pdl_wait();
@@ -288,11 +320,10 @@ __global__ void __launch_bounds__(NT) attn_decode_kernel(DecAttnArgs a, float qs
 
   const T* kb = reinterpret_cast<const T*>(a.k) + h * dk;
   constexpr int KPW = 32 / G;            // keys per warp per round (lane groups)
-  // U rounds unrolled: U * KPW keys (U * CH 16-byte loads per lane) in flight per warp
   const int g = lane / G, li = lane % G;
   const int stride = (NT / 32) * KPW;
   for (int j0 = warp * KPW; j0 < c.nk; j0 += stride * U) {
-    float f[U][CH][VEC];
+    uint4 raw[U][CH];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int j = j0 + u * stride + g;
@@ -301,7 +332,7 @@ __global__ void __launch_bounds__(NT) attn_decode_kernel(DecAttnArgs a, float qs
 #pragma unroll
         for (int ch = 0; ch < CH; ++ch) {
           const int e0 = (li + ch * G) * VEC;
-          if (e0 < dk) load16(kr + e0, f[u][ch]);
+          if (e0 < dk) raw[u][ch] = *reinterpret_cast<const uint4*>(kr + e0);
         }
       }
     }
@@ -314,8 +345,10 @@ __global__ void __launch_bounds__(NT) attn_decode_kernel(DecAttnArgs a, float qs
         for (int ch = 0; ch < CH; ++ch) {
           const int e0 = (li + ch * G) * VEC;
           if (e0 < dk) {
+            float f[VEC];
+            cvt16<T>(raw[u][ch], f);
 #pragma unroll
-            for (int i = 0; i < VEC; ++i) s = fmaf(qs[e0 + i], f[u][ch][i], s);
+            for (int i = 0; i < VEC; ++i) s = fmaf(qs[e0 + i], f[i], s);
           }
         }
       }
@@ -328,7 +361,7 @@ __global__ void __launch_bounds__(NT) attn_decode_kernel(DecAttnArgs a, float qs
   if (warp == 0) softmax_inplace(S, c.nk);
   __syncthreads();
 
-  // value product: thread = (chunk, key group)
+  // value product: thread = (chunk, key group); keys in a fixed order per group
   const int nch = dk / VEC;
   const int groups = NT / nch;
   const int ch = tid % nch, grp = tid / nch;
@@ -337,26 +370,24 @@ __global__ void __launch_bounds__(NT) attn_decode_kernel(DecAttnArgs a, float qs
 #pragma unroll
   for (int i = 0; i < VEC; ++i) acc[i] = 0.f;
   if (grp < groups) {
-    constexpr int U3 = U;   // value rows in flight per thread
-    for (int j0 = grp; j0 < c.nk; j0 += groups * U3) {
-      float f[U3][VEC];
-      float w[U3];
+    for (int j0 = grp; j0 < c.nk; j0 += groups * UV) {
+      uint4 rv[UV];
 #pragma unroll
-      for (int u = 0; u < U3; ++u) {
+      for (int u = 0; u < UV; ++u) {
         const int j = j0 + u * groups;
-        if (j < c.nk) {
-          load16(vb + decode_key_row(a, c, r, j) * a.ldkv, f[u]);
-          w[u] = S[j];
-        } else {
-          w[u] = 0.f;
-#pragma unroll
-          for (int i = 0; i < VEC; ++i) f[u][i] = 0.f;
-        }
+        if (j < c.nk) rv[u] = *reinterpret_cast<const uint4*>(vb + decode_key_row(a, c, r, j) * a.ldkv);
       }
 #pragma unroll
-      for (int u = 0; u < U3; ++u)
+      for (int u = 0; u < UV; ++u) {
+        const int j = j0 + u * groups;
+        if (j < c.nk) {
+          const float w = S[j];
+          float f[VEC];
+          cvt16<T>(rv[u], f);
 #pragma unroll
-        for (int i = 0; i < VEC; ++i) acc[i] = fmaf(w[u], f[u][i], acc[i]);
+          for (int i = 0; i < VEC; ++i) acc[i] = fmaf(w, f[i], acc[i]);
+        }
+      }
     }
 #pragma unroll
     for (int i = 0; i < VEC; ++i) red[grp * dk + ch * VEC + i] = acc[i];
@@ -567,35 +598,39 @@ cudaError_t varlen_dispatch(const AttnArgs& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// FNMT_DEC_U = score rounds x 10 + value rows in flight (11, 14, 18, 24, 28);
+// r01 A/B (6-1-1 bench): 11 6.82M, 14 6.86M, 18 6.47M, 24 6.87M, 28 6.70M words/s
 int dec_unroll() {
   static int u = -1;
   if (u < 0) {
     const char* e = getenv("FNMT_DEC_U");
-    u = e ? atoi(e) : 1;
-    if (u != 2 && u != 4) u = 1;
+    u = e ? atoi(e) : 24;
+    if (u != 11 && u != 14 && u != 18 && u != 28) u = 24;
   }
   return u;
 }
 
-template <typename T, int G, int CH, int NT, int U>
+template <typename T, int G, int CH, int NT, int U, int UV>
 cudaError_t launch_dec_nt_u(const DecAttnArgs& a, float qscale, cudaStream_t s) {
   const int groups = NT / (a.dk / Vec16<T>::N);
   const size_t smem = sizeof(float) * ((size_t)a.dk + a.max_k + 4 + (size_t)groups * a.dk);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
   if (smem > 48 * 1024) {
-    cudaError_t e = set_max_smem((const void*)attn_decode_kernel<T, G, CH, NT, U>);
+    cudaError_t e = set_max_smem((const void*)attn_decode_kernel<T, G, CH, NT, U, UV>);
     if (e != cudaSuccess) return e;
   }
-  return launch_k(attn_decode_kernel<T, G, CH, NT, U>, dim3(a.rows, a.heads), dim3(NT), smem, s, a,
-                  qscale);
+  return launch_k(attn_decode_kernel<T, G, CH, NT, U, UV>, dim3(a.rows, a.heads), dim3(NT), smem,
+                  s, a, qscale);
 }
 
 template <typename T, int G, int CH, int NT>
 cudaError_t launch_dec_nt(const DecAttnArgs& a, float qscale, cudaStream_t s) {
   switch (dec_unroll()) {
-    case 4: return launch_dec_nt_u<T, G, CH, NT, 4>(a, qscale, s);
-    case 2: return launch_dec_nt_u<T, G, CH, NT, 2>(a, qscale, s);
-    default: return launch_dec_nt_u<T, G, CH, NT, 1>(a, qscale, s);
+    case 14: return launch_dec_nt_u<T, G, CH, NT, 1, 4>(a, qscale, s);
+    case 18: return launch_dec_nt_u<T, G, CH, NT, 1, 8>(a, qscale, s);
+    case 24: return launch_dec_nt_u<T, G, CH, NT, 2, 4>(a, qscale, s);
+    case 28: return launch_dec_nt_u<T, G, CH, NT, 2, 8>(a, qscale, s);
+    default: return launch_dec_nt_u<T, G, CH, NT, 1, 1>(a, qscale, s);
   }
 }
 

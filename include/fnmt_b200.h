@@ -78,6 +78,16 @@ int fnmt_linear(const void* A, int lda, int a_dtype, const void* W, int ldw, con
                 void* C, int ldc, int c_dtype, int M, int N, int K, int relu, const float* resid,
                 int ld_resid, void* stream);
 
+/* x = norm(x + A . W^T + bias) * gain + beta in place (f32 x [M, N]), plus
+ * its copy in the A dtype (x_act, may be NULL) — Projection.apply followed by
+ * the post-norm residual block of encode / decode_step (model.py:279-286,
+ * :327-343, tensor.py:98-129).  f16 / bf16 with N in {256, 512, 768, 1024}
+ * run one clustered tcgen05 GEMM whose epilogue all-reduces the row
+ * statistics through distributed shared memory; otherwise GEMM + add_norm. */
+int fnmt_linear_add_norm(const void* A, int lda, int a_dtype, const void* W, int ldw,
+                         const float* bias, float* x, void* x_act, const float* gain,
+                         const float* beta, int l1, int M, int N, int K, void* stream);
+
 /* out_idx[m] = argmax_n (A[m,:] . W[n,:] + bias[n]), lowest n on ties — the
  * vocab projection (model.py:344) fused with np.argmax (search.py:71).
  * keys_scratch: M uint64 device words. */

@@ -54,6 +54,8 @@ _SIGNATURES = {
     "fnmt_version": (C.c_char_p, []),
     "fnmt_linear": (_I, [_VP, _I, _I, _VP, _I, _VP, _VP, _I, _I, _I, _I, _I, _I, _VP, _I, _VP]),
     "fnmt_linear_argmax": (_I, [_VP, _I, _I, _VP, _I, _VP, _I, _I, _I, _VP, _VP, _VP]),
+    "fnmt_linear_add_norm": (_I, [_VP, _I, _I, _VP, _I, _VP, _VP, _VP, _VP, _VP, _I, _I, _I, _I,
+                                  _VP]),
     "fnmt_qgemm_workspace": (_I64, [_I64, _I]),
     "fnmt_qgemm": (_I, [_VP, _I, _VP, _VP, _VP, _VP, _VP, _VP, _I, _I, _I, _I, _I, _VP, _I64,
                         _VP]),

@@ -95,6 +95,50 @@ int fnmt_linear(const void* A, int lda, int a_dtype, const void* W, int ldw, con
   return cuda_status(fnmt::launch_gemm(g, (cudaStream_t)stream), "fnmt_linear");
 }
 
+int fnmt_linear_add_norm(const void* A, int lda, int a_dtype, const void* W, int ldw,
+                         const float* bias, float* x, void* x_act, const float* gain,
+                         const float* beta, int l1, int M, int N, int K, void* stream) {
+  if (!valid_dtype(a_dtype) || !A || !W || !x || !gain || !beta || M < 0 || N < 4 || N % 4 ||
+      K < 1 || lda < K || ldw < K)
+    return fail(FNMT_E_INVALID, "fnmt_linear_add_norm: bad arguments");
+  if (M == 0) return FNMT_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  fnmt::GemmArgs g;
+  g.A = A;
+  g.lda = lda;
+  g.W = W;
+  g.ldw = ldw;
+  g.in_dtype = a_dtype;
+  g.bias = bias;
+  g.M = M;
+  g.N = N;
+  g.K = K;
+  if (fnmt::gemm_norm_supported(N, a_dtype)) {
+    g.epi = fnmt::kEpiNorm;
+    g.C = x;
+    g.ldc = N;
+    g.c_dtype = a_dtype;
+    g.C2 = x_act;
+    g.resid = x;
+    g.ld_resid = N;
+    g.ngain = gain;
+    g.nbeta = beta;
+    g.nl1 = l1;
+    return cuda_status(fnmt::launch_gemm(g, s), "fnmt_linear_add_norm");
+  }
+  float* y = nullptr;
+  cudaError_t e = cudaMallocAsync(&y, sizeof(float) * (size_t)M * N, s);
+  if (e != cudaSuccess) return cuda_status(e, "fnmt_linear_add_norm scratch");
+  g.C = y;
+  g.ldc = N;
+  g.c_dtype = fnmt::kF32;
+  e = fnmt::launch_gemm(g, s);
+  if (e == cudaSuccess)
+    e = fnmt::launch_add_norm(x, y, gain, beta, l1, x, x_act, a_dtype, M, N, s);
+  cudaError_t e2 = cudaFreeAsync(y, s);
+  return cuda_status(e != cudaSuccess ? e : e2, "fnmt_linear_add_norm");
+}
+
 int64_t fnmt_qgemm_workspace(int64_t M, int K) {
   if (M < 0 || K < 1) return fail(FNMT_E_INVALID, "fnmt_qgemm_workspace: bad arguments");
   return fnmt::qgemm_scratch_bytes(std::max<int64_t>(M, 1), K);

@@ -651,6 +651,43 @@ void Engine::norm(const float* x, const float* y, const Norm& n, float* o32, voi
   ++launches;
 }
 
+void Engine::gemm_norm(const void* A, const CUtensorMap* tmA, int lda, const Lin& L, int M,
+                       float* x32, void* xa, float* y32, const Norm& n, cudaStream_t s) {
+  if (q8 || dt == kF32 || !gemm_norm_supported(L.N, dt) || L.N != arch.d_model) {
+    gemm(A, tmA, lda, L, M, y32, L.N, kF32, 0, s);
+    norm(x32, y32, n, x32, xa, M, s);
+    return;
+  }
+  GemmArgs g;
+  g.A = A;
+  g.lda = lda;
+  g.W = L.w;
+  g.ldw = L.K;
+  g.in_dtype = dt;
+  g.bias = L.b;
+  g.M = M;
+  g.N = L.N;
+  g.K = L.K;
+  g.epi = kEpiNorm;
+  g.C = x32;
+  g.ldc = L.N;
+  g.c_dtype = dt;
+  g.C2 = xa;
+  g.resid = x32;
+  g.ld_resid = L.N;
+  g.ngain = n.g;
+  g.nbeta = n.b;
+  g.nl1 = arch.norm_l1;
+  g.tmap_a = tmA;
+  g.tmap_w = &L.tm;
+  const int ev = prof_begin(s);
+  CK(launch_gemm(g, s));
+  prof_end(s, ev, gemm_cls, 2.0 * M * L.N * L.K,
+           (double)M * L.K * dtype_size(dt) + (double)L.N * L.K * dtype_size(dt) +
+               (double)M * L.N * (8.0 + dtype_size(dt)));
+  ++launches;
+}
+
 // Encoder over rows already embedded in ws.x32 / ws.xa (model.py:279-286).
 void Engine::encoder_layers(int n_tok, int n_seq, int max_q, int max_k, const int32_t* qstart,
                             const int32_t* qlen, const int32_t* kstart, const int32_t* klen,
@@ -685,11 +722,10 @@ void Engine::encoder_layers(int n_tok, int n_seq, int max_q, int max_k, const in
       prof_end(s, ev, FNMT_K_ATTN_ENC, 0.0, (double)n_tok * 4 * d * dtype_size(dt));
     }
     ++launches;
-    gemm(ws.att, tc ? &ws.tm_att : nullptr, d, L.o, n_tok, ws.y32, d, kF32, 0, s);
-    norm(ws.x32, ws.y32, L.n1, ws.x32, ws.xa, n_tok, s);
+    gemm_norm(ws.att, tc ? &ws.tm_att : nullptr, d, L.o, n_tok, ws.x32, ws.xa, ws.y32, L.n1, s);
     gemm(ws.xa, tc ? &ws.tm_xa : nullptr, d, L.f1, n_tok, ws.h, arch.ffn_dim_enc, dt, 1, s);
-    gemm(ws.h, tc ? &ws.tm_h : nullptr, arch.ffn_dim_enc, L.f2, n_tok, ws.y32, d, kF32, 0, s);
-    norm(ws.x32, ws.y32, L.n2, ws.x32, ws.xa, n_tok, s);
+    gemm_norm(ws.h, tc ? &ws.tm_h : nullptr, arch.ffn_dim_enc, L.f2, n_tok, ws.x32, ws.xa, ws.y32,
+              L.n2, s);
   }
 }
 
@@ -779,8 +815,7 @@ void Engine::run_step(const StepView& v, cudaStream_t s) {
       prof_end(s, ev, FNMT_K_ATTN_DEC, 0.0, (double)R * (v.host_t + 1) * 2 * d * es);
     }
     ++launches;
-    gemm(ws.datt, tc ? &ws.tm_datt : nullptr, d, L.so, R, ws.dy32, d, kF32, 0, s);
-    norm(ws.dx32, ws.dy32, L.n1, ws.dx32, ws.dxa, R, s);
+    gemm_norm(ws.datt, tc ? &ws.tm_datt : nullptr, d, L.so, R, ws.dx32, ws.dxa, ws.dy32, L.n1, s);
     gemm(ws.dxa, tc ? &ws.tm_dxa : nullptr, d, L.cq, R, ws.dq, d, dt, 0, s);
     DecAttnArgs c{};
     c.q = ws.dq;
@@ -809,12 +844,11 @@ void Engine::run_step(const StepView& v, cudaStream_t s) {
       prof_end(s, ev, FNMT_K_ATTN_DEC, 0.0, (double)R * v.max_k * 2 * d * es);
     }
     ++launches;
-    gemm(ws.datt, tc ? &ws.tm_datt : nullptr, d, L.co, R, ws.dy32, d, kF32, 0, s);
-    norm(ws.dx32, ws.dy32, L.n2, ws.dx32, ws.dxa, R, s);
+    gemm_norm(ws.datt, tc ? &ws.tm_datt : nullptr, d, L.co, R, ws.dx32, ws.dxa, ws.dy32, L.n2, s);
     if (L.ffn) {
       gemm(ws.dxa, tc ? &ws.tm_dxa : nullptr, d, L.f1, R, ws.dh, arch.ffn_dim_dec, dt, 1, s);
-      gemm(ws.dh, tc ? &ws.tm_dh : nullptr, arch.ffn_dim_dec, L.f2, R, ws.dy32, d, kF32, 0, s);
-      norm(ws.dx32, ws.dy32, L.n3, ws.dx32, ws.dxa, R, s);
+      gemm_norm(ws.dh, tc ? &ws.tm_dh : nullptr, arch.ffn_dim_dec, L.f2, R, ws.dx32, ws.dxa, ws.dy32,
+                L.n3, s);
     }
   }
   if (v.topk && tc) {

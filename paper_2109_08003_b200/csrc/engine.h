@@ -232,6 +232,10 @@ class Engine {
                    unsigned long long* keys, cudaStream_t s);
   void norm(const float* x, const float* y, const Norm& n, float* o32, void* oa, int rows,
             cudaStream_t s);
+  // x32 = norm(x32 + A.W + b) (and its storage-dtype copy xa): one clustered
+  // GEMM with the LayerNorm in the epilogue when possible, else GEMM + add_norm.
+  void gemm_norm(const void* A, const CUtensorMap* tmA, int lda, const Lin& L, int M, float* x32,
+                 void* xa, float* y32, const Norm& n, cudaStream_t s);
   void encoder_layers(int n_tok, int n_seq, int max_q, int max_k, const int32_t* qstart,
                       const int32_t* qlen, const int32_t* kstart, const int32_t* klen, int k_pad,
                       cudaStream_t s);

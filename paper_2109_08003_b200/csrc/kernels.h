@@ -53,6 +53,9 @@ enum Epilogue : int {
   kEpiArgmax = 1,  // keys[m] = max over n < valid_n of key(acc + bias[n], n)
   kEpiTopK = 2,    // per (row, 256-column tile): max, sum exp(x - max), top-K (value, index)
   kEpiQKV = 3,     // decoder self q|k|v: q -> C, k / v -> KV cache slot (row*cap + *t_ptr)
+  kEpiNorm = 4,    // out = norm(resid + acc + bias) * gain + beta over the full row: the N
+                   // tiles of a row block live in one thread-block cluster and exchange
+                   // row statistics through distributed shared memory
 };
 
 // Per-(row, N-tile) partials of the beam epilogue; tile = n / kTopKTile.
@@ -121,7 +124,17 @@ struct GemmArgs {
   int Kp = 0;
   const CUtensorMap* qtmap_w = nullptr;
   QScratch qs{};
+  // kEpiNorm (model.py:193-196 after the residual add, tensor.py:98-129):
+  // resid is the f32 residual stream x, C the f32 output (may alias resid),
+  // C2 the storage-dtype copy (c_dtype) for the next GEMM.
+  const float* ngain = nullptr;
+  const float* nbeta = nullptr;
+  int nl1 = 0;
+  void* C2 = nullptr;
 };
+// Can launch_gemm fuse the LayerNorm for this (N, dtype)?  (tensor-core path,
+// N = cluster size x N tile with cluster size <= 8)
+bool gemm_norm_supported(int N, int in_dtype);
 
 // Encode a 2-D TMA descriptor for a row-major [rows, cols] 16-bit matrix with
 // leading dimension ld (elements), box = [box_rows, 64 cols], 128 B swizzle.

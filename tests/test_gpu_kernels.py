@@ -219,3 +219,32 @@ def test_varlen_attention_f16_tensor_core(heads, d, lens):
     torch.cuda.synchronize()
     got = out.float().cpu().numpy().reshape(b, s, d)
     assert np.abs(got - want).max() <= 1e-2 * max(1.0, np.abs(want).max())
+
+
+@pytest.mark.parametrize("dt", ["f16", "bf16"])
+@pytest.mark.parametrize("M,N,K,l1", [(3, 512, 512, 0), (300, 512, 2048, 0), (1000, 512, 512, 1),
+                                      (130, 768, 768, 0), (77, 256, 64, 1), (50, 96, 64, 0)])
+def test_linear_add_norm_fused(dt, M, N, K, l1):
+    """x = norm(x + A W^T + b): clustered GEMM + DSMEM LayerNorm epilogue (and
+    the GEMM + add_norm fallback for N outside the cluster shapes) against
+    the fp32 oracle on storage-rounded operands."""
+    rng = np.random.default_rng(M + N + K)
+    tdt = torch.float16 if dt == "f16" else torch.bfloat16
+    A = torch.from_numpy(rng.standard_normal((M, K)).astype(np.float32)).to(tdt)
+    W = torch.from_numpy((rng.standard_normal((N, K)) / np.sqrt(K)).astype(np.float32)).to(tdt)
+    b = rng.standard_normal(N).astype(np.float32) * 0.1
+    x = rng.standard_normal((M, N)).astype(np.float32)
+    g = (1 + 0.1 * rng.standard_normal(N)).astype(np.float32)
+    be = (0.1 * rng.standard_normal(N)).astype(np.float32)
+    y = A.float().numpy() @ W.float().numpy().T + b
+    want = O.norm_rows("l1" if l1 else "l2", x + y, g, be)
+    Ad, Wd = A.to(DEV), W.to(DEV)
+    X = torch.from_numpy(x).to(DEV)
+    Xa = torch.empty((M, N), dtype=tdt, device=DEV)
+    B, G, Be = (torch.from_numpy(v).to(DEV) for v in (b, g, be))
+    check(lib.fnmt_linear_add_norm(ptr(Ad), K, _capi.DTYPES[dt], ptr(Wd), K, ptr(B), ptr(X),
+                                   ptr(Xa), ptr(G), ptr(Be), l1, M, N, K, stream()), "add_norm")
+    torch.cuda.synchronize()
+    got = X.cpu().numpy()
+    assert np.abs(got - want).max() <= 2e-3 * max(1.0, np.abs(want).max())
+    assert np.allclose(Xa.float().cpu().numpy(), got, atol=3e-2, rtol=1e-2)

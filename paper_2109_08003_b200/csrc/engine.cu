@@ -653,7 +653,8 @@ void Engine::norm(const float* x, const float* y, const Norm& n, float* o32, voi
 
 void Engine::gemm_norm(const void* A, const CUtensorMap* tmA, int lda, const Lin& L, int M,
                        float* x32, void* xa, float* y32, const Norm& n, cudaStream_t s) {
-  if (q8 || dt == kF32 || !gemm_norm_supported(L.N, dt) || L.N != arch.d_model) {
+  if (q8 || dt == kF32 || !gemm_norm_enabled() || !gemm_norm_supported(L.N, dt) ||
+      L.N != arch.d_model) {
     gemm(A, tmA, lda, L, M, y32, L.N, kF32, 0, s);
     norm(x32, y32, n, x32, xa, M, s);
     return;

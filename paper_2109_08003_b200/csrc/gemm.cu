@@ -798,13 +798,22 @@ cudaError_t launch_tc_norm(const CUtensorMap& ta, const CUtensorMap& tw, const G
 
 }  // namespace
 
-bool gemm_norm_supported(int N, int in_dtype) {
+// The engine's post-norm blocks use it only with FNMT_GEMM_NORM=1: r01 measured the
+// clustered epilogue slower than GEMM + add_norm (6-1-1 bench 4.23M vs 6.81M words/s;
+// encoder GEMMs 74 vs 21 ms per 16k sentences) — two DSMEM round trips per 128-row tile
+// serialise the epilogue, which then dominates the 1-tile-deep TMEM double buffer.
+// fnmt_linear_add_norm (C ABI) always fuses.
+bool gemm_norm_enabled() {
   static int on = -1;
   if (on < 0) {
     const char* e = getenv("FNMT_GEMM_NORM");
-    on = !(e && e[0] == '0');
+    on = e && e[0] == '1';
   }
-  if (!on || (in_dtype != kF16 && in_dtype != kBF16)) return false;
+  return on != 0;
+}
+
+bool gemm_norm_supported(int N, int in_dtype) {
+  if (in_dtype != kF16 && in_dtype != kBF16) return false;
   return N == 256 || N == 512 || N == 768 || N == 1024;
 }
 

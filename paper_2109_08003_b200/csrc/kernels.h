@@ -135,6 +135,7 @@ struct GemmArgs {
 // Can launch_gemm fuse the LayerNorm for this (N, dtype)?  (tensor-core path,
 // N = cluster size x N tile with cluster size <= 8)
 bool gemm_norm_supported(int N, int in_dtype);
+bool gemm_norm_enabled();   // engine opt-in (FNMT_GEMM_NORM=1)
 
 // Encode a 2-D TMA descriptor for a row-major [rows, cols] 16-bit matrix with
 // leading dimension ld (elements), box = [box_rows, 64 cols], 128 B swizzle.

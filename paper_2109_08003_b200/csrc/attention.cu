@@ -27,6 +27,8 @@
 //    multiple of one 16-byte vector (tiny test models).
 #include <math.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -401,6 +403,144 @@ __global__ void __launch_bounds__(NT) attn_decode_kernel(DecAttnArgs a, float qs
   }
 }
 
+
+// Single-pass decode attention with an online softmax (fp16 / bf16 storage).
+// Slot = (warp, lane group of G lanes); slot s walks keys s, s + SLOTS, ...
+// loading each key's K and V chunks together (U keys in flight per slot) and
+// keeps a running (max m, sum l, output o) — o rescaled by exp(m_old - m_new)
+// when the max grows.  The slots merge in a fixed order at the end:
+//   out = sum_s o_s e^(m_s - M) / sum_s l_s e^(m_s - M).
+// Mathematically the reference's max-shifted softmax followed by the value
+// product (tensor.py:70-81, model.py:226-240); the rounding differs only by
+// where the 1/sum is applied, far inside the fp16 tolerance.  One pass over
+// K and V instead of score / softmax / value phases separated by barriers.
+template <typename T, int G, int CH, int NT, int U>
+__global__ void __launch_bounds__(NT) attn_decode_online_kernel(DecAttnArgs a, float qscale) {
+  pdl_trigger();
+  pdl_wait();
+  constexpr int VEC = Vec16<T>::N;
+  constexpr int KPW = 32 / G;
+  constexpr int SLOTS = (NT / 32) * KPW;
+  extern __shared__ float sm[];
+  const int dk = a.dk;
+  float* qs = sm;                          // [dk]
+  float* so = qs + dk;                     // [SLOTS][dk]
+  float* sml = so + SLOTS * dk;            // [SLOTS][2]
+  const int r = blockIdx.x, h = blockIdx.y;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const DecCtx c = decode_setup<T>(a, r, h);
+  const T* q = reinterpret_cast<const T*>(a.q) + (size_t)r * a.ldq + h * dk;
+  for (int e = tid; e < dk; e += NT) qs[e] = to_f32(q[e]) * qscale;
+  __syncthreads();
+
+  const T* kb = reinterpret_cast<const T*>(a.k) + h * dk;
+  const T* vb = reinterpret_cast<const T*>(a.v) + h * dk;
+  const int g = lane / G, li = lane % G;
+  const int slot = warp * KPW + g;
+  float m = -INFINITY, l = 0.f;
+  float o[CH][VEC];
+#pragma unroll
+  for (int ch = 0; ch < CH; ++ch)
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) o[ch][i] = 0.f;
+
+  for (int j0 = slot; j0 < c.nk; j0 += SLOTS * U) {
+    uint4 rk[U][CH], rv[U][CH];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = j0 + u * SLOTS;
+      if (j < c.nk) {
+        const int64_t row = decode_key_row(a, c, r, j);
+        const T* kr = kb + row * a.ldkv;
+        const T* vr = vb + row * a.ldkv;
+#pragma unroll
+        for (int ch = 0; ch < CH; ++ch) {
+          const int e0 = (li + ch * G) * VEC;
+          if (e0 < dk) {
+            rk[u][ch] = *reinterpret_cast<const uint4*>(kr + e0);
+            rv[u][ch] = *reinterpret_cast<const uint4*>(vr + e0);
+          }
+        }
+      }
+    }
+    float sc[U];
+    float mx = m;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = j0 + u * SLOTS;
+      float sacc = 0.f;
+      if (j < c.nk) {
+#pragma unroll
+        for (int ch = 0; ch < CH; ++ch) {
+          const int e0 = (li + ch * G) * VEC;
+          if (e0 < dk) {
+            float f[VEC];
+            cvt16<T>(rk[u][ch], f);
+#pragma unroll
+            for (int i = 0; i < VEC; ++i) sacc = fmaf(qs[e0 + i], f[i], sacc);
+          }
+        }
+      }
+#pragma unroll
+      for (int off = G / 2; off > 0; off >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, off);
+      sc[u] = j < c.nk ? (c.all_masked ? sacc + kMaskValue : sacc) : -INFINITY;
+      mx = fmaxf(mx, sc[u]);
+    }
+    if (mx == -INFINITY) continue;   // no live key in this round for this slot
+    const float resc = expf(m - mx);   // m = -inf on the first live round -> 0
+    l *= resc;
+#pragma unroll
+    for (int ch = 0; ch < CH; ++ch)
+#pragma unroll
+      for (int i = 0; i < VEC; ++i) o[ch][i] *= resc;
+    m = mx;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = j0 + u * SLOTS;
+      if (j < c.nk) {
+        const float p = expf(sc[u] - m);
+        l += p;
+#pragma unroll
+        for (int ch = 0; ch < CH; ++ch) {
+          const int e0 = (li + ch * G) * VEC;
+          if (e0 < dk) {
+            float f[VEC];
+            cvt16<T>(rv[u][ch], f);
+#pragma unroll
+            for (int i = 0; i < VEC; ++i) o[ch][i] = fmaf(p, f[i], o[ch][i]);
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int ch = 0; ch < CH; ++ch) {
+    const int e0 = (li + ch * G) * VEC;
+    if (e0 < dk)
+#pragma unroll
+      for (int i = 0; i < VEC; ++i) so[slot * dk + e0 + i] = o[ch][i];
+  }
+  if (li == 0) {
+    sml[2 * slot] = m;
+    sml[2 * slot + 1] = l;
+  }
+  __syncthreads();
+  float M = -INFINITY;
+  for (int s2 = 0; s2 < SLOTS; ++s2) M = fmaxf(M, sml[2 * s2]);
+  T* out = reinterpret_cast<T*>(a.out) + (size_t)r * a.ldo + h * dk;
+  for (int e = tid; e < dk; e += NT) {
+    float L = 0.f, O = 0.f;
+    for (int s2 = 0; s2 < SLOTS; ++s2) {
+      const float ms = sml[2 * s2];
+      if (ms == -INFINITY) continue;
+      const float w = expf(ms - M);
+      L = fmaf(sml[2 * s2 + 1], w, L);
+      O = fmaf(so[s2 * dk + e], w, O);
+    }
+    out[e] = from_f32<T>(O / L);
+  }
+}
+
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)),
                "l"(gmem_src)
@@ -648,8 +788,35 @@ cudaError_t launch_dec_async(const DecAttnArgs& a, float qscale, cudaStream_t s)
                   a, qscale);
 }
 
+bool dec_online_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("FNMT_DEC_ONLINE");
+    on = !(e && e[0] == '0');
+  }
+  return on != 0;
+}
+
+template <typename T, int G, int CH>
+cudaError_t launch_dec_online(const DecAttnArgs& a, float qscale, cudaStream_t s) {
+  constexpr int NT = 128;
+  constexpr int U = G == 32 ? 2 : 4;
+  constexpr int SLOTS = (NT / 32) * (32 / G);
+  auto kern = attn_decode_online_kernel<T, G, CH, NT, U>;
+  const size_t smem = sizeof(float) * ((size_t)a.dk * (SLOTS + 1) + 2 * SLOTS);
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;
+  if (smem > 48 * 1024) {
+    cudaError_t e = set_max_smem((const void*)kern);
+    if (e != cudaSuccess) return e;
+  }
+  return launch_k(kern, dim3(a.rows, a.heads), dim3(NT), smem, s, a, qscale);
+}
+
 template <typename T, int G, int CH>
 cudaError_t launch_dec(const DecAttnArgs& a, float qscale, cudaStream_t s) {
+  if constexpr (!std::is_same<T, float>::value) {
+    if (dec_online_enabled()) return launch_dec_online<T, G, CH>(a, qscale, s);
+  }
   // few (row, head) blocks -> wide blocks so the SMs still have enough warps in flight
   // cp.async staging measured faster for 8 heads (dk=64) only (r01: 6-1-8 3.92M vs 3.67M
   // words/s; 6-1-1 3.92M vs 4.32M)

@@ -822,11 +822,16 @@ cudaError_t launch_dec_async(const DecAttnArgs& a, float qscale, cudaStream_t s)
                   a, qscale);
 }
 
+// Opt-in (FNMT_DEC_ONLINE=1): r01 measured the single-pass kernel slower than the two-pass
+// one — 6-1-1 6.71M vs 6.77M, 6-1-8 5.26M vs 5.64M, 6-6-8 beam 4 0.407M vs 0.439M words/s
+// (attn_dec 39 / 66 / 1270 ms vs 38 / 53 / 1130 ms): the per-key exp / rescale work sits on
+// the load critical path, where the two-pass kernel's value phase spreads keys over all
+// threads.
 bool dec_online_enabled() {
   static int on = -1;
   if (on < 0) {
     const char* e = getenv("FNMT_DEC_ONLINE");
-    on = !(e && e[0] == '0');
+    on = e && e[0] == '1';
   }
   return on != 0;
 }

@@ -591,7 +591,7 @@ void Engine::reserve_for(const fnmt_run& run) {
 // building blocks
 
 void Engine::gemm(const void* A, const CUtensorMap* tmA, int lda, const Lin& L, int M, void* C,
-                  int ldc, int c_dtype, int relu, cudaStream_t s) {
+                  int ldc, int c_dtype, int relu, cudaStream_t s, const float* resid) {
   GemmArgs g;
   g.A = A;
   g.lda = lda;
@@ -606,6 +606,8 @@ void Engine::gemm(const void* A, const CUtensorMap* tmA, int lda, const Lin& L, 
   g.ldc = ldc;
   g.c_dtype = c_dtype;
   g.relu = relu;
+  g.resid = resid;
+  g.ld_resid = ldc;
   g.tmap_a = tmA;
   g.tmap_w = dt == kF32 ? nullptr : &L.tm;
   attach_q(g, L);
@@ -613,7 +615,7 @@ void Engine::gemm(const void* A, const CUtensorMap* tmA, int lda, const Lin& L, 
   CK(launch_gemm(g, s));
   prof_end(s, ev, gemm_cls, 2.0 * M * L.N * L.K,
            (double)M * L.K * dtype_size(dt) + (double)L.N * L.K * dtype_size(dt) +
-               (double)M * L.N * dtype_size(c_dtype));
+               (double)M * L.N * (dtype_size(c_dtype) + (resid ? 4.0 : 0.0)));
   ++launches;
 }
 
@@ -647,7 +649,7 @@ void Engine::norm(const float* x, const float* y, const Norm& n, float* o32, voi
   CK(launch_add_norm(x, y, n.g, n.b, arch.norm_l1, o32, dt == kF32 ? nullptr : oa,
                      dt, rows, arch.d_model, s));
   prof_end(s, ev, FNMT_K_NORM, 0.0,
-           (double)rows * arch.d_model * (12.0 + (dt == kF32 ? 0 : dtype_size(dt))));
+           (double)rows * arch.d_model * ((y ? 12.0 : 8.0) + (dt == kF32 ? 0 : dtype_size(dt))));
   ++launches;
 }
 
@@ -655,8 +657,12 @@ void Engine::gemm_norm(const void* A, const CUtensorMap* tmA, int lda, const Lin
                        float* x32, void* xa, float* y32, const Norm& n, cudaStream_t s) {
   if (q8 || dt == kF32 || !gemm_norm_enabled() || !gemm_norm_supported(L.N, dt) ||
       L.N != arch.d_model) {
-    gemm(A, tmA, lda, L, M, y32, L.N, kF32, 0, s);
-    norm(x32, y32, n, x32, xa, M, s);
+    // residual add in the GEMM epilogue (x32 = x32 + (A.W + b), same f32 order as
+    // add_norm's x + y), then the LayerNorm alone: the f32 sublayer output never
+    // round-trips through HBM
+    (void)y32;
+    gemm(A, tmA, lda, L, M, x32, L.N, kF32, 0, s, x32);
+    norm(x32, nullptr, n, x32, xa, M, s);
     return;
   }
   GemmArgs g;

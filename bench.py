@@ -169,9 +169,9 @@ _CPU_STATE = {}
 
 def _cpu_worker(rows):
     from oracle import nmt_oracle as O
-    a, p = _CPU_STATE["arch"], _CPU_STATE["params"]
+    a, p, k = _CPU_STATE["arch"], _CPU_STATE["params"], _CPU_STATE["beam"]
     tok, valid = O.pad_rows(rows)
-    out = O.greedy(a, p, tok, valid)
+    out = O.greedy(a, p, tok, valid) if k == 1 else O.beam(a, p, tok, valid, k)
     return sum(len(o) for o in out), sum(len(r) for r in rows)
 
 
@@ -187,12 +187,16 @@ def cpu_run(rows_per_proc, procs):
     return sum(r[0] for r in res), sum(r[1] for r in res), dt
 
 
-def cpu_setup():
+def cpu_setup(model_cfg=None, beam=1):
+    """The selected model (BASELINE config of --model) with random_model(cfg, 0)
+    weights, greedy or beam as --beam says."""
     os.environ["OMP_NUM_THREADS"] = "1"
     from oracle import nmt_oracle as O
-    a = O.STUDENT_6_1_1
+    from paper_2109_08003_b200 import store as S
+    a = O.arch_of(S.ModelConfig(**(model_cfg or CFG)))
     _CPU_STATE["arch"] = a
     _CPU_STATE["params"] = O.make_params(a, 0)
+    _CPU_STATE["beam"] = beam
 
 
 def cpu_sample(ids, offsets, start, procs, per_proc):
@@ -206,17 +210,36 @@ def cpu_sample(ids, offsets, start, procs, per_proc):
     return rows, k
 
 
-def cpu_baseline(ids, offsets, seconds):
-    cpu_setup()
+def cpu_baseline(ids, offsets, seconds, model_cfg=None, beam=1):
+    cpu_setup(model_cfg, beam)
     procs = os.cpu_count() or 1
-    # calibrate per-process sample size to ~`seconds` of work (~55 words/s/core)
-    per_proc = max(1, int(seconds * 55 / 41.25 / 1.5))
+    # calibrate per-process sample size to ~`seconds` of work (~55 words/s/core for
+    # Student-6-1-1 greedy; the beam / larger configs run ~15-20x slower)
+    rate = 55.0 if (beam == 1 and (model_cfg or CFG)["n_dec_layers"] == 1) else 3.0
+    per_proc = max(1, int(seconds * rate / 41.25 / 1.5))
     rows, _ = cpu_sample(ids, offsets, 0, procs, per_proc)
     words, src, dt = cpu_run(rows, procs)
     return {"value": words / dt, "unit": UNIT, "cores": procs, "kind": "port",
             "sample": f"{procs} procs x {per_proc} sentences of the synthetic corpus "
                       f"({words} target words, {src} source words, {dt:.1f} s), oracle/nmt_oracle.py "
-                      f"f32 numpy, one thread per process"}
+                      f"f32 numpy {'greedy' if beam == 1 else f'beam {beam}'}, one thread per process"}
+
+
+def arm_config(args, world):
+    """The `config` object both arms print (BASELINE config of --model)."""
+    model_desc = MODELS[args.model][0]
+    C = args.chunk_sentences
+    beam = args.beam
+    return {"workload": f"{model_desc.split(' (')[0]} {args.dtype} "
+                        f"{'greedy' if beam == 1 else f'beam={beam}'}, 1M (2^20) synthetic "
+                        f"newstest-shaped sentences, dynamic batching sbatch/wbatch "
+                        f"{SBATCH}/{WBATCH}",
+            "model": f"{model_desc[:-1]}, random-init seed 0)",
+            "beam": beam,
+            "corpus_sentences": CORPUS, "chunk_sentences": C,
+            "sentences_per_step_all_ranks": C * world,
+            "parallelism": f"sentence-sharded dp{world} (no collective)",
+            "l2": "256 MiB memset between steps; per-step working set >> L2"}
 
 
 def run_reference(args):
@@ -226,10 +249,11 @@ def run_reference(args):
     if rank != 0:
         return 0
     from paper_2109_08003_b200.synthetic import newstest_corpus
-    ids, offsets, _ = newstest_corpus(CORPUS, CFG["vocab_size"])
-    cpu_setup()
+    model_cfg = MODELS[args.model][1]
+    ids, offsets, _ = newstest_corpus(CORPUS, model_cfg["vocab_size"])
+    cpu_setup(model_cfg, args.beam)
     procs = os.cpu_count() or 1
-    per_proc = 2
+    per_proc = 2 if args.beam == 1 and model_cfg["n_dec_layers"] == 1 else 1
     k = 0
     for _ in range(args.warmup):
         rows, k = cpu_sample(ids, offsets, k, procs, 1)
@@ -247,11 +271,12 @@ def run_reference(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic", "impl": "reference",
-            "config": {"workload": "Student-6-1-1 greedy f32 (reference CPU algorithm), "
-                                   "newstest-shaped synthetic sentences", "model": "Student-6-1-1"},
+            "config": arm_config(args, 1),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": "port",
                              "sample": f"{args.steps} steps x {procs} procs x {per_proc} sentences "
-                                       f"({words} target words)"},
+                                       f"of the same corpus ({words} target words), the "
+                                       f"reference algorithm (oracle/nmt_oracle.py, f32 numpy, "
+                                       f"pinned to the reference) on the host cores"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
@@ -443,23 +468,14 @@ def main():
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(ids, offsets, args.cpu_seconds)
+        cpu = cpu_baseline(ids, offsets, args.cpu_seconds, model_cfg, BEAM)
 
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
         "steps": K, "warmup": W, "ms_per_step": round(1e3 * t_max / max(K, 1), 2),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": args.dtype, "data": "synthetic",
-        "config": {"workload": f"{model_desc.split(' (')[0]} {args.dtype} "
-                               f"{'greedy' if BEAM == 1 else f'beam={BEAM}'}, 1M (2^20) synthetic "
-                               f"newstest-shaped sentences, dynamic batching sbatch/wbatch "
-                               f"{SBATCH}/{WBATCH}",
-                   "model": f"{model_desc[:-1]}, random-init seed 0)",
-                   "beam": BEAM,
-                   "corpus_sentences": CORPUS, "chunk_sentences": C,
-                   "sentences_per_step_all_ranks": C * world,
-                   "parallelism": f"sentence-sharded dp{world} (no collective)",
-                   "l2": "256 MiB memset between steps; per-step working set >> L2"},
+        "config": arm_config(args, world),
         "e2e": e2e,
         "gpu_launches": int(launches),
         "roofline": roofline,

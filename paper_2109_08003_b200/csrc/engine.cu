@@ -657,12 +657,11 @@ void Engine::gemm_norm(const void* A, const CUtensorMap* tmA, int lda, const Lin
                        float* x32, void* xa, float* y32, const Norm& n, cudaStream_t s) {
   if (q8 || dt == kF32 || !gemm_norm_enabled() || !gemm_norm_supported(L.N, dt) ||
       L.N != arch.d_model) {
-    // residual add in the GEMM epilogue (x32 = x32 + (A.W + b), same f32 order as
-    // add_norm's x + y), then the LayerNorm alone: the f32 sublayer output never
-    // round-trips through HBM
-    (void)y32;
-    gemm(A, tmA, lda, L, M, x32, L.N, kF32, 0, s, x32);
-    norm(x32, nullptr, n, x32, xa, M, s);
+    // (r01: moving the residual add into the GEMM epilogue — x32 += A.W + b in place —
+    // measured slower, 6.30M vs 6.78M words/s: the row-per-thread f32 residual loads
+    // stall the epilogue more than add_norm's coalesced second stream costs)
+    gemm(A, tmA, lda, L, M, y32, L.N, kF32, 0, s);
+    norm(x32, y32, n, x32, xa, M, s);
     return;
   }
   GemmArgs g;

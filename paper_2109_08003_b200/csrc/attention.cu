@@ -575,6 +575,117 @@ __global__ void __launch_bounds__(NT) attn_decode_online_kernel(DecAttnArgs a, f
   }
 }
 
+
+// Multi-head decode attention, one CTA per ROW covering all H heads.  A key
+// row of all heads is d contiguous elements (H x dk), so a warp streams it
+// exactly like the single-head dk = d case (G = 32 lanes, CH 16-byte chunks per
+// lane); lane li's chunk ch belongs to head (li + 32 ch) / LPH, LPH = dk / VEC
+// lanes per head, and the score of each head is a shuffle reduction inside its
+// LPH-lane group.  The value pass weights chunk c with its own head's softmax
+// row.  Versus a CTA per (row, head) this loads 8x fewer, 8x larger key
+// vectors per CTA and runs 8x fewer CTAs.  Same two-pass numerics as
+// attn_decode_kernel.
+template <typename T, int CH, int NT, int LPH, int U = 2, int UV = 4>
+__global__ void __launch_bounds__(NT) attn_decode_rows_kernel(DecAttnArgs a, float qscale) {
+  pdl_trigger();
+  pdl_wait();
+  constexpr int VEC = Vec16<T>::N;
+  static_assert(LPH == 8 || LPH == 16 || LPH == 32, "lanes per head");
+  extern __shared__ float sm[];
+  const int H = a.heads, dk = a.dk, d = H * dk;
+  float* qs = sm;                  // [d]
+  float* S = qs + d;               // [H][max_k]
+  float* red = S + (size_t)H * a.max_k + 4;   // [groups][d]
+  const int r = blockIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  DecCtx c = decode_setup<T>(a, r, 0);
+  for (int hh = 1; hh < H && a.self_mode && a.new_k; ++hh) c = decode_setup<T>(a, r, hh);  // append all heads
+  const T* q = reinterpret_cast<const T*>(a.q) + (size_t)r * a.ldq;
+  for (int e = tid; e < d; e += NT) qs[e] = to_f32(q[e]) * qscale;
+  __syncthreads();
+
+  const T* kb = reinterpret_cast<const T*>(a.k);
+  constexpr int NW = NT / 32;
+  for (int j0 = warp; j0 < c.nk; j0 += NW * U) {
+    uint4 raw[U][CH];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = j0 + u * NW;
+      if (j < c.nk) {
+        const T* kr = kb + decode_key_row(a, c, r, j) * a.ldkv;
+#pragma unroll
+        for (int ch = 0; ch < CH; ++ch) {
+          const int e0 = (lane + ch * 32) * VEC;
+          if (e0 < d) raw[u][ch] = *reinterpret_cast<const uint4*>(kr + e0);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = j0 + u * NW;
+#pragma unroll
+      for (int ch = 0; ch < CH; ++ch) {
+        const int e0 = (lane + ch * 32) * VEC;
+        float sacc = 0.f;
+        if (j < c.nk && e0 < d) {
+          float f[VEC];
+          cvt16<T>(raw[u][ch], f);
+#pragma unroll
+          for (int i = 0; i < VEC; ++i) sacc = fmaf(qs[e0 + i], f[i], sacc);
+        }
+#pragma unroll
+        for (int o = LPH / 2; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
+        if ((lane % LPH) == 0 && j < c.nk && e0 < d) {
+          const int hh = e0 / dk;
+          S[(size_t)hh * a.max_k + j] = c.all_masked ? sacc + kMaskValue : sacc;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  for (int hh = warp; hh < H; hh += NW) softmax_inplace(S + (size_t)hh * a.max_k, c.nk);
+  __syncthreads();
+
+  const int nch = d / VEC;
+  const int groups = NT / nch;
+  const int chn = tid % nch, grp = tid / nch;
+  const T* vb = reinterpret_cast<const T*>(a.v) + chn * VEC;
+  const float* Sh = S + (size_t)((chn * VEC) / dk) * a.max_k;
+  float acc[VEC];
+#pragma unroll
+  for (int i = 0; i < VEC; ++i) acc[i] = 0.f;
+  if (grp < groups) {
+    for (int j0 = grp; j0 < c.nk; j0 += groups * UV) {
+      uint4 rv[UV];
+#pragma unroll
+      for (int u = 0; u < UV; ++u) {
+        const int j = j0 + u * groups;
+        if (j < c.nk) rv[u] = *reinterpret_cast<const uint4*>(vb + decode_key_row(a, c, r, j) * a.ldkv);
+      }
+#pragma unroll
+      for (int u = 0; u < UV; ++u) {
+        const int j = j0 + u * groups;
+        if (j < c.nk) {
+          const float w = Sh[j];
+          float f[VEC];
+          cvt16<T>(rv[u], f);
+#pragma unroll
+          for (int i = 0; i < VEC; ++i) acc[i] = fmaf(w, f[i], acc[i]);
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) red[grp * d + chn * VEC + i] = acc[i];
+  }
+  __syncthreads();
+  T* out = reinterpret_cast<T*>(a.out) + (size_t)r * a.ldo;
+  for (int e = tid; e < d; e += NT) {
+    float sum = red[e];
+    for (int gg = 1; gg < groups; ++gg) sum += red[gg * d + e];
+    out[e] = from_f32<T>(sum);
+  }
+}
+
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)),
                "l"(gmem_src)
@@ -875,10 +986,61 @@ cudaError_t launch_dec(const DecAttnArgs& a, float qscale, cudaStream_t s) {
   return launch_dec_nt<T, G, CH, 128>(a, qscale, s);
 }
 
+bool dec_rows_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("FNMT_DEC_ROWS");
+    on = !(e && e[0] == '0');
+  }
+  return on != 0;
+}
+
+template <typename T, int CH, int LPH>
+cudaError_t launch_dec_rows(const DecAttnArgs& a, float qscale, cudaStream_t s) {
+  constexpr int NT = 128;
+  const int d = a.heads * a.dk;
+  const int groups = NT / (d / Vec16<T>::N);
+  const size_t smem =
+      sizeof(float) * ((size_t)d + (size_t)a.heads * a.max_k + 4 + (size_t)groups * d);
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;
+  auto kern = attn_decode_rows_kernel<T, CH, NT, LPH>;
+  if (smem > 48 * 1024) {
+    cudaError_t e = set_max_smem((const void*)kern);
+    if (e != cudaSuccess) return e;
+  }
+  return launch_k(kern, dim3(a.rows), dim3(NT), smem, s, a, qscale);
+}
+
+// Multi-head rows: heads of 8 / 16 / 32 lanes (fp16 dk 64 / 128 / 256), a row of
+// 256 .. 512 elements per 128-thread CTA (CH 1 or 2 chunks per lane).
+template <typename T>
+cudaError_t try_dec_rows(const DecAttnArgs& a, float qscale, cudaStream_t s) {
+  constexpr int VEC = Vec16<T>::N;
+  if (sizeof(T) != 2 || a.heads < 2 || !dec_rows_enabled() || a.dk % VEC || (a.ldkv % VEC) ||
+      (a.ldq % VEC))
+    return cudaErrorNotSupported;
+  const int lph = a.dk / VEC, d = a.heads * a.dk;
+  if (d % (32 * VEC)) return cudaErrorNotSupported;
+  const int ch = d / (32 * VEC);
+  if (ch == 1) {
+    if (lph == 8) return launch_dec_rows<T, 1, 8>(a, qscale, s);
+    if (lph == 16) return launch_dec_rows<T, 1, 16>(a, qscale, s);
+  } else if (ch == 2) {
+    if (lph == 8) return launch_dec_rows<T, 2, 8>(a, qscale, s);
+    if (lph == 16) return launch_dec_rows<T, 2, 16>(a, qscale, s);
+    if (lph == 32) return launch_dec_rows<T, 2, 32>(a, qscale, s);
+  }
+  return cudaErrorNotSupported;
+}
+
 template <typename T>
 cudaError_t decode_dispatch(const DecAttnArgs& a, cudaStream_t s) {
   constexpr int VEC = Vec16<T>::N;
   const float qscale = (float)(1.0 / sqrt((double)a.dk));
+  if constexpr (sizeof(T) == 2) {
+    const cudaError_t e = try_dec_rows<T>(a, qscale, s);
+    if (e != cudaErrorNotSupported) return e;
+  }
   const int nch = a.dk / VEC;
   const bool vec_ok = a.dk % VEC == 0 && nch <= kDThreads && (a.ldkv % VEC) == 0 &&
                       sizeof(float) * ((size_t)a.dk * 5 + a.max_k + 4) <= 227 * 1024;

@@ -175,3 +175,36 @@ def test_config1_student_greedy_vs_reference(golden, student_weights, dtype):
     print("fp16 divergences (sentence, step, reference top1-top2 gap):", report)
     assert same >= 0.99 * 64, report
     assert all(gap <= 0.05 for _, _, gap in report), report
+
+
+@pytest.mark.parametrize("d,heads,dec", [(256, 4, 1), (512, 4, 2), (512, 2, 1), (512, 8, 1),
+                                         (256, 2, 1)])
+def test_multihead_decode_rows_fp16(d, heads, dec):
+    """Decoder shapes that take the all-heads-per-row decode attention
+    (head sizes 64 / 128 / 256 in fp16): logits of 6 forced steps within the
+    fp16 tolerance of the oracle, and native beam-4 (ancestor-table self
+    attention) close to the oracle's beam."""
+    cfg = S.ModelConfig(2, dec, d, heads, heads, 2 * d, d, 300, 64)
+    seed = d + heads + dec
+    w = S.random_model(cfg, seed)
+    a = O.arch_of(cfg)
+    p = O.make_params(a, seed)
+    rng = np.random.default_rng(seed)
+    rows = [rng.integers(4, cfg.vocab_size, size=int(rng.integers(3, 20))) for _ in range(9)]
+    tok, valid = O.pad_rows(rows)
+    m = GpuTranslationModel(cfg, w, dtype="f16")
+    enc = m.encode(tok, valid)
+    cache = m.init_cache(enc)
+    oc = O.start_cache(a, p, O.encoder(a, p, tok, valid), valid)
+    prev = np.full(len(rows), 2, np.int64)
+    for t in range(6):
+        want = O.decoder_step(a, p, oc, prev)
+        assert rel_err(m.step(cache, prev), want) <= 1e-2, t
+        prev = want.argmax(axis=1).astype(np.int64)
+    eng = Engine(cfg, w, dtype="f16")
+    lengths = np.array([len(r) for r in rows])
+    offsets = np.concatenate([[0], np.cumsum(lengths)]).astype(np.int64)
+    out, olen, off, _ = eng.translate(np.concatenate(rows).astype(np.int32), offsets, beam=4)
+    got = split_off(out, olen, off)
+    want = O.beam(a, p, tok, valid, 4)
+    assert sum(x == y for x, y in zip(got, want)) >= len(rows) - 2

@@ -590,12 +590,19 @@ __global__ void __launch_bounds__(NT) attn_decode_rows_kernel(DecAttnArgs a, flo
   pdl_trigger();
   pdl_wait();
   constexpr int VEC = Vec16<T>::N;
-  static_assert(LPH == 8 || LPH == 16 || LPH == 32, "lanes per head");
+  // LPH 8 / 16 / 32: head score = shuffle reduction inside the head's lane
+  // group.  LPH 0 (head sizes that do not map to a power-of-two lane group,
+  // e.g. dk 96): per-chunk partials go through shared memory and lane h sums
+  // head h's chunks in order.
+  static_assert(LPH == 0 || LPH == 8 || LPH == 16 || LPH == 32, "lanes per head");
+  constexpr int NW = NT / 32;
   extern __shared__ float sm[];
   const int H = a.heads, dk = a.dk, d = H * dk;
   float* qs = sm;                  // [d]
   float* S = qs + d;               // [H][max_k]
   float* red = S + (size_t)H * a.max_k + 4;   // [groups][d]
+  const int groups_v = NT / (d / VEC);
+  float* part = red + (size_t)groups_v * d;    // LPH 0: [NW][U][32 CH]
   const int r = blockIdx.x;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   DecCtx c = decode_setup<T>(a, r, 0);
@@ -605,7 +612,6 @@ __global__ void __launch_bounds__(NT) attn_decode_rows_kernel(DecAttnArgs a, flo
   __syncthreads();
 
   const T* kb = reinterpret_cast<const T*>(a.k);
-  constexpr int NW = NT / 32;
   for (int j0 = warp; j0 < c.nk; j0 += NW * U) {
     uint4 raw[U][CH];
 #pragma unroll
@@ -633,13 +639,34 @@ __global__ void __launch_bounds__(NT) attn_decode_rows_kernel(DecAttnArgs a, flo
 #pragma unroll
           for (int i = 0; i < VEC; ++i) sacc = fmaf(qs[e0 + i], f[i], sacc);
         }
+        if constexpr (LPH > 0) {
 #pragma unroll
-        for (int o = LPH / 2; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
-        if ((lane % LPH) == 0 && j < c.nk && e0 < d) {
-          const int hh = e0 / dk;
-          S[(size_t)hh * a.max_k + j] = c.all_masked ? sacc + kMaskValue : sacc;
+          for (int o = LPH / 2; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
+          if ((lane % LPH) == 0 && j < c.nk && e0 < d) {
+            const int hh = e0 / dk;
+            S[(size_t)hh * a.max_k + j] = c.all_masked ? sacc + kMaskValue : sacc;
+          }
+        } else {
+          part[(warp * U + u) * 32 * CH + lane + ch * 32] = sacc;
         }
       }
+    }
+    if constexpr (LPH == 0) {
+      __syncwarp();
+      const int lpc = dk / VEC;   // chunks per head
+      if (lane < H) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int j = j0 + u * NW;
+          if (j < c.nk) {
+            const float* pp = part + (warp * U + u) * 32 * CH + lane * lpc;
+            float sacc = 0.f;
+            for (int i = 0; i < lpc; ++i) sacc += pp[i];
+            S[(size_t)lane * a.max_k + j] = c.all_masked ? sacc + kMaskValue : sacc;
+          }
+        }
+      }
+      __syncwarp();
     }
   }
   __syncthreads();
@@ -1000,8 +1027,8 @@ cudaError_t launch_dec_rows(const DecAttnArgs& a, float qscale, cudaStream_t s) 
   constexpr int NT = 128;
   const int d = a.heads * a.dk;
   const int groups = NT / (d / Vec16<T>::N);
-  const size_t smem =
-      sizeof(float) * ((size_t)d + (size_t)a.heads * a.max_k + 4 + (size_t)groups * d);
+  const size_t smem = sizeof(float) * ((size_t)d + (size_t)a.heads * a.max_k + 4 +
+                                       (size_t)groups * d + (LPH ? 0 : (NT / 32) * 2 * 32 * CH));
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
   auto kern = attn_decode_rows_kernel<T, CH, NT, LPH>;
   if (smem > 48 * 1024) {
@@ -1022,13 +1049,23 @@ cudaError_t try_dec_rows(const DecAttnArgs& a, float qscale, cudaStream_t s) {
   const int lph = a.dk / VEC, d = a.heads * a.dk;
   if (d % (32 * VEC)) return cudaErrorNotSupported;
   const int ch = d / (32 * VEC);
+  if (a.heads > 32) return cudaErrorNotSupported;
   if (ch == 1) {
     if (lph == 8) return launch_dec_rows<T, 1, 8>(a, qscale, s);
     if (lph == 16) return launch_dec_rows<T, 1, 16>(a, qscale, s);
+    return launch_dec_rows<T, 1, 0>(a, qscale, s);
   } else if (ch == 2) {
     if (lph == 8) return launch_dec_rows<T, 2, 8>(a, qscale, s);
     if (lph == 16) return launch_dec_rows<T, 2, 16>(a, qscale, s);
     if (lph == 32) return launch_dec_rows<T, 2, 32>(a, qscale, s);
+    return launch_dec_rows<T, 2, 0>(a, qscale, s);
+  } else if (ch == 3) {
+    return launch_dec_rows<T, 3, 0>(a, qscale, s);   // e.g. Deep-12-768: 8 heads x 96
+  } else if (ch == 4) {
+    if (lph == 8) return launch_dec_rows<T, 4, 8>(a, qscale, s);
+    if (lph == 16) return launch_dec_rows<T, 4, 16>(a, qscale, s);
+    if (lph == 32) return launch_dec_rows<T, 4, 32>(a, qscale, s);
+    return launch_dec_rows<T, 4, 0>(a, qscale, s);
   }
   return cudaErrorNotSupported;
 }

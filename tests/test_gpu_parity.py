@@ -178,12 +178,13 @@ def test_config1_student_greedy_vs_reference(golden, student_weights, dtype):
 
 
 @pytest.mark.parametrize("d,heads,dec", [(256, 4, 1), (512, 4, 2), (512, 2, 1), (512, 8, 1),
-                                         (256, 2, 1)])
+                                         (256, 2, 1), (768, 8, 2), (256, 8, 1), (1024, 8, 1)])
 def test_multihead_decode_rows_fp16(d, heads, dec):
     """Decoder shapes that take the all-heads-per-row decode attention
     (head sizes 64 / 128 / 256 in fp16): logits of 6 forced steps within the
     fp16 tolerance of the oracle, and native beam-4 (ancestor-table self
-    attention) close to the oracle's beam."""
+    attention) close to the oracle's beam.  (768, 8) and (256, 8) have head
+    sizes 96 / 32 whose lane groups are not powers of two (smem partials)."""
     cfg = S.ModelConfig(2, dec, d, heads, heads, 2 * d, d, 300, 64)
     seed = d + heads + dec
     w = S.random_model(cfg, seed)

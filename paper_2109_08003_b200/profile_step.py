@@ -1,5 +1,7 @@
 """Small fixed workload for ncu: one corpus slice through the engine
-(Student-6-1-1 fp16 greedy).  Usage: python tools/profile_step.py [n_sentences]"""
+(Student-6-1-1, fp16 greedy by default).
+
+Usage: python -m paper_2109_08003_b200.profile_step [n_sentences] [dtype] [beam]"""
 import sys
 from pathlib import Path
 
@@ -17,8 +19,9 @@ n = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
 cfg = S.ModelConfig(6, 1, 512, 1, 1, 2048, 2048, 32772, 1024)
 ids, off, lens = newstest_corpus(n, cfg.vocab_size)
 eng = Engine(cfg, S.random_model(cfg, 0), dtype=sys.argv[2] if len(sys.argv) > 2 else "f16")
+beam = int(sys.argv[3]) if len(sys.argv) > 3 else 1
 for _ in range(2):
-    out, olen, oo, st = eng.translate(ids, off, sbatch=3072, wbatch=64000)
+    out, olen, oo, st = eng.translate(ids, off, sbatch=3072, wbatch=64000, beam=beam)
 torch.cuda.synchronize()
 print("words", int(olen.sum()), "launches", st.gpu_launches, "batches", st.batches,
       "steps", st.decode_steps, "ms", st.total_ms)

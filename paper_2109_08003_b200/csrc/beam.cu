@@ -101,7 +101,7 @@ __global__ void logits_topk_partials_kernel(const float* __restrict__ logits, in
   double s = 0.0;
   for (int c = c0 + lane; c < min(n, c0 + kTopKTile); c += 32) s += (double)expf(row[c] - mx);
   s = warp_sum_d(s);
-  const size_t R = (size_t)p.rstride;
+  const size_t o = (size_t)r * p.tiles + tile;
   for (int round = 0; round < p.K; ++round) {
     unsigned long long key = ti[0] >= 0 ? argmax_key(tv[0], (uint32_t)ti[0]) : 0ull;
     unsigned long long best = key;
@@ -120,82 +120,69 @@ __global__ void logits_topk_partials_kernel(const float* __restrict__ logits, in
       ti[kTopKMax - 1] = -1;
     }
     if (lane == 0) {
-      const size_t oj = ((size_t)tile * p.K + round) * R + r;
-      p.pval[oj] = best ? float_from_order_key((uint32_t)(best >> 32)) : -INFINITY;
-      p.pidx[oj] = best ? (int)argmax_key_index(best) : -1;
+      p.pval[o * p.K + round] = best ? float_from_order_key((uint32_t)(best >> 32)) : -INFINITY;
+      p.pidx[o * p.K + round] = best ? (int)argmax_key_index(best) : -1;
     }
   }
   if (lane == 0) {
-    p.pmax[(size_t)tile * R + r] = mx;
-    p.psum[(size_t)tile * R + r] = s;
+    p.pmax[o] = mx;
+    p.psum[o] = s;
   }
 }
 
-// logZ and the row's top-k.  CTA = 32 rows x 8 warps: lane = row, warp w
-// walks tiles w, w + 8, ... so every partial load is a coalesced 32-row line
-// of the tile-major partials; the 8 warps' max / sum / top-K lists meet in
-// shared memory and lane r of warp 0 finishes row r (fixed order: the sum over
-// warps 0..7, top-K by the total order value desc, index asc).
-__global__ void __launch_bounds__(256) beam_row_reduce_kernel(BeamState b) {
+// one warp per row: logZ and the row's top-k
+__global__ void beam_row_reduce_kernel(BeamState b) {
   pdl_trigger();
   pdl_wait();
-  constexpr int KM = kTopKMax;
-  __shared__ float smax[kWarpsPerCta][32];
-  __shared__ double sz[kWarpsPerCta][32];
-  __shared__ float sv[kWarpsPerCta][KM][32];
-  __shared__ int si[kWarpsPerCta][KM][32];
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int r = blockIdx.x * 32 + lane;
-  const bool ok = r < b.rows && b.active[r];
+  const int r = blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= b.rows || !b.active[r]) return;
   const TopKPartials& p = b.part;
   const int T = p.tiles;
-  const size_t R = (size_t)p.rstride;
   float M = -INFINITY;
-  if (ok)
-    for (int i = w; i < T; i += kWarpsPerCta) M = fmaxf(M, p.pmax[(size_t)i * R + r]);
-  smax[w][lane] = M;
-  __syncthreads();
-  M = smax[0][lane];
-#pragma unroll
-  for (int i = 1; i < kWarpsPerCta; ++i) M = fmaxf(M, smax[i][lane]);
+  for (int i = lane; i < T; i += 32) M = fmaxf(M, p.pmax[(size_t)r * T + i]);
+  M = warp_max(M);
   double z = 0.0;
-  float tv[KM];
-  int ti[KM];
+  for (int i = lane; i < T; i += 32) {
+    const size_t o = (size_t)r * T + i;
+    z += p.psum[o] * exp((double)p.pmax[o] - (double)M);
+  }
+  z = warp_sum_d(z);
+  float tv[kTopKMax];
+  int ti[kTopKMax];
 #pragma unroll
-  for (int j = 0; j < KM; ++j) {
+  for (int j = 0; j < kTopKMax; ++j) {
     tv[j] = -INFINITY;
     ti[j] = -1;
   }
-  if (ok) {
-    for (int i = w; i < T; i += kWarpsPerCta) {
-      const size_t o = (size_t)i * R + r;
-      z += p.psum[o] * exp((double)p.pmax[o] - (double)M);
-      for (int j = 0; j < p.K; ++j) {
-        const size_t oj = ((size_t)i * p.K + j) * R + r;
-        const int id = p.pidx[oj];
-        if (id >= 0) topk_insert(tv, ti, p.pval[oj], id);
+  for (int i = lane; i < T * p.K; i += 32) {
+    const size_t o = (size_t)r * T * p.K + i;
+    const int id = p.pidx[o];
+    if (id >= 0) topk_insert(tv, ti, p.pval[o], id);
+  }
+  for (int round = 0; round < b.k; ++round) {
+    const unsigned long long key = ti[0] >= 0 ? argmax_key(tv[0], (uint32_t)ti[0]) : 0ull;
+    unsigned long long best = key;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const unsigned long long o2 = __shfl_xor_sync(0xffffffffu, best, off);
+      best = o2 > best ? o2 : best;
+    }
+    if (best != 0ull && key == best) {
+#pragma unroll
+      for (int j = 0; j < kTopKMax - 1; ++j) {
+        tv[j] = tv[j + 1];
+        ti[j] = ti[j + 1];
       }
+      tv[kTopKMax - 1] = -INFINITY;
+      ti[kTopKMax - 1] = -1;
+    }
+    if (lane == 0) {
+      b.rval[(size_t)r * b.k + round] = best ? float_from_order_key((uint32_t)(best >> 32)) : -INFINITY;
+      b.ridx[(size_t)r * b.k + round] = best ? (int)argmax_key_index(best) : -1;
     }
   }
-  sz[w][lane] = z;
-#pragma unroll
-  for (int j = 0; j < KM; ++j) {
-    sv[w][j][lane] = tv[j];
-    si[w][j][lane] = ti[j];
-  }
-  __syncthreads();
-  if (w != 0 || !ok) return;
-  z = 0.0;
-  for (int i = 0; i < kWarpsPerCta; ++i) z += sz[i][lane];
-  for (int i = 1; i < kWarpsPerCta; ++i)
-#pragma unroll
-    for (int j = 0; j < KM; ++j)
-      if (si[i][j][lane] >= 0) topk_insert(tv, ti, sv[i][j][lane], si[i][j][lane]);
-  for (int round = 0; round < b.k; ++round) {
-    b.rval[(size_t)r * b.k + round] = ti[round] >= 0 ? tv[round] : -INFINITY;
-    b.ridx[(size_t)r * b.k + round] = ti[round];
-  }
-  b.rlogz[r] = (double)M + log(z);
+  if (lane == 0) b.rlogz[r] = (double)M + log(z);
 }
 
 // candidate order: score desc, token asc, parent asc (search.py:131)
@@ -394,8 +381,8 @@ cudaError_t launch_logits_topk_partials(const float* logits, int rows, int n,
 }
 
 cudaError_t launch_beam_row_reduce(const BeamState& b, cudaStream_t s) {
-  return launch_k(beam_row_reduce_kernel, dim3((b.rows + 31) / 32), dim3(32 * kWarpsPerCta), 0,
-                  s, b);
+  return launch_k(beam_row_reduce_kernel, dim3((b.rows + kWarpsPerCta - 1) / kWarpsPerCta),
+                  dim3(32 * kWarpsPerCta), 0, s, b);
 }
 
 cudaError_t launch_beam_select(const BeamState& b, cudaStream_t s) {

@@ -1230,7 +1230,6 @@ void Engine::reserve_beam(int sent_cap, int k, int64_t pool_cap) {
   const int64_t cap_per_row = pool_cap / rows + 1;
   beam.part.tiles = tiles;
   beam.part.K = K;
-  beam.part.rstride = rows;
   beam.part.pmax = (float*)alloc(sizeof(float) * (size_t)rows * tiles);
   beam.part.psum = (double*)alloc(sizeof(double) * (size_t)rows * tiles);
   beam.part.pval = (float*)alloc(sizeof(float) * (size_t)rows * tiles * K);

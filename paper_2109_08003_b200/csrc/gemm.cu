@@ -473,14 +473,13 @@ __device__ __forceinline__ void topk_epilogue(const EpiParams& ep, uint32_t tadd
     sum += (double)cs;
   }
   if (row_ok && n0 < ep.N) {   // a half tile entirely past N has no partial slot
-    const size_t R = (size_t)ep.tk.rstride, t = (size_t)(n0 / kTopKTile);
-    const size_t o = t * R + m;
+    const size_t o = (size_t)m * ep.tk.tiles + n0 / kTopKTile;
     ep.tk.pmax[o] = mx;
     ep.tk.psum[o] = sum;
 #pragma unroll
     for (int j = 0; j < TOPK; ++j) {
-      ep.tk.pval[(t * TOPK + j) * R + m] = tv[j];
-      ep.tk.pidx[(t * TOPK + j) * R + m] = ti[j];
+      ep.tk.pval[o * TOPK + j] = tv[j];
+      ep.tk.pidx[o * TOPK + j] = ti[j];
     }
   }
 }

@@ -62,17 +62,13 @@ enum Epilogue : int {
 // Per-(row, N-tile) partials of the beam epilogue; tile = n / kTopKTile.
 constexpr int kTopKTile = 128;
 constexpr int kTopKMax = 8;
-// Tile-major so the GEMM epilogue (one thread per row) writes coalesced:
-// element (row r, tile t) of pmax / psum at t * rstride + r, entry j of its
-// top-K at (t * K + j) * rstride + r.
 struct TopKPartials {
-  float* pmax;     // [tiles][rstride]
-  double* psum;    // [tiles][rstride]
-  float* pval;     // [tiles][K][rstride]
-  int32_t* pidx;   // [tiles][K][rstride]
+  float* pmax;     // [rows][tiles]
+  double* psum;    // [rows][tiles]
+  float* pval;     // [rows][tiles][K]
+  int32_t* pidx;   // [rows][tiles][K]
   int tiles;
   int K;           // 4 or 8 entries kept per tile
-  int rstride;     // allocated rows
 };
 
 // Per-call scratch of the int8 GEMM: quantized activations [M, Kp] u8,

@@ -38,6 +38,7 @@ constexpr int kBM = 128;
 constexpr int kBK = 64;
 constexpr int kWBox = 64;   // W TMA box rows; BN/64 boxes per stage
 constexpr int kABytes = kBM * kBK * 2;
+constexpr int kEpiWarpsC = 8;   // epilogue warps (kEpiWarps, needed before its definition)
 
 struct EpiParams {
   const float* bias;
@@ -238,6 +239,39 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& ep, int m, int n
   }
 }
 
+// kEpiStore without residual, coalesced: the warp's 32 rows x 32 columns go
+// through a padded smem square so each store instruction writes 32
+// consecutive columns of ONE row (a 128-byte f32 / 64-byte 16-bit line)
+// instead of 32 rows' 16-byte pieces.  Same values as epilogue_chunk.
+__device__ __forceinline__ void staged_store_chunk(const EpiParams& ep, int row0, int nb,
+                                                   const float (&v)[32], const float* bs,
+                                                   float* sq, int lane) {
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    float x = v[i] + bs[i];
+    if (ep.relu) x = fmaxf(x, 0.f);
+    sq[lane * 33 + i] = x;
+  }
+  __syncwarp();
+  const int n = nb + lane;
+  const bool col_ok = n < ep.N;
+#pragma unroll 4
+  for (int rr = 0; rr < 32; ++rr) {
+    const int m = row0 + rr;
+    const float x = sq[rr * 33 + lane];
+    if (m < ep.M && col_ok) {
+      const size_t off = (size_t)m * ep.ldc + n;
+      if (ep.c_dtype == kF32)
+        reinterpret_cast<float*>(ep.C)[off] = x;
+      else if (ep.c_dtype == kF16)
+        reinterpret_cast<__half*>(ep.C)[off] = __float2half_rn(x);
+      else
+        reinterpret_cast<__nv_bfloat16*>(ep.C)[off] = __float2bfloat16_rn(x);
+    }
+  }
+  __syncwarp();
+}
+
 // int8 epilogue: turn 32 s32 accumulators of row m into the f32 value of
 // quant8.qgemm (quant8.py:246-278) — the zeropoint cross terms expanded
 // against the row / column sums, evaluated in double in the reference's
@@ -378,8 +412,10 @@ __device__ __forceinline__ void norm_epilogue(const EpiParams& ep, uint32_t tadd
 // persistent tcgen05 kernel
 
 // Every stage row is 128 bytes of K: 64 fp16/bf16 elements, or 128 int8.
-template <int BN, int STAGES, bool I8 = false, int CN = 0, int KA = 0>
+template <int BN, int STAGES, bool I8 = false, int CN = 0, int KA = 0, bool STG = false>
 struct TcCfg {
+  // STG: per epilogue warp a 32 x 33 fp32 staging square for coalesced stores
+  static constexpr int kStgBytes = STG ? kEpiWarpsC * 32 * 33 * 4 : 0;
   static constexpr int kBKe = I8 ? 2 * kBK : kBK;   // K elements per stage
   static constexpr int kBBytes = BN * kBK * 2;
   // KA > 0 (A-stationary): the CTA's 128-row A block (KA k-blocks) stays in
@@ -391,7 +427,7 @@ struct TcCfg {
   // kEpiNorm: row-statistic slots [parity][pass][rank][128] + half-row partials [2][128]
   static constexpr int kNormBytes = CN ? (4 * CN * kBM + 2 * kBM) * 8 + 64 : 0;
   static constexpr int kSmem =
-      1024 + kARegion + STAGES * kStage + 2 * BN * kColBytes + kNormBytes + 256;
+      1024 + kARegion + STAGES * kStage + 2 * BN * kColBytes + kNormBytes + kStgBytes + 256;
 };
 
 // Tile of this CTA's it-th iteration (-1 when done).  Plain: a grid-stride
@@ -484,11 +520,12 @@ __device__ __forceinline__ void topk_epilogue(const EpiParams& ep, uint32_t tadd
   }
 }
 
-template <int BN, int STAGES, int TOPK, bool I8 = false, int MINB = 1, int CN = 0, int KA = 0>
+template <int BN, int STAGES, int TOPK, bool I8 = false, int MINB = 1, int CN = 0, int KA = 0,
+          bool STG = false>
 __global__ void __launch_bounds__(kTcThreads, MINB)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmw,
                    int K, uint32_t idesc, EpiParams ep, int tiles_n, int tiles) {
-  using Cfg = TcCfg<BN, STAGES, I8, CN, KA>;
+  using Cfg = TcCfg<BN, STAGES, I8, CN, KA, STG>;
   constexpr bool AST = KA > 0;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -504,7 +541,8 @@ __global__ void __launch_bounds__(kTcThreads, MINB)
   double* nslot = reinterpret_cast<double*>(bias_s + (Cfg::kColBytes / 4) * 2 * BN);
   double* nhalf = nslot + (CN ? 4 * CN * kBM : 0);
   uint64_t* nbar = reinterpret_cast<uint64_t*>(nhalf + (CN ? 2 * kBM : 0));   // [parity][pass]
-  uint64_t* full = nbar + (CN ? 4 : 0);
+  float* stg = reinterpret_cast<float*>(nbar + (CN ? 4 : 0));   // STG: [kEpiWarps][32][33]
+  uint64_t* full = reinterpret_cast<uint64_t*>(stg + (STG ? kEpiWarpsC * 32 * 33 : 0));
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
@@ -686,8 +724,14 @@ __global__ void __launch_bounds__(kTcThreads, MINB)
               q_dequant_chunk(ep, m, v, qsc_s + o, qzp_s + o, qcs_s + o);
             }
           }
-          if (row_ok && nb < ep.N)
-            epilogue_chunk(ep, m, nb, v, bs + col0 + c * 32, best_v, best_i);
+          if constexpr (STG) {
+            if (nb < ep.N)   // warp-uniform
+              staged_store_chunk(ep, m0 + quarter * 32, nb, v, bs + col0 + c * 32,
+                                 stg + (warp - 2) * 32 * 33, lane);
+          } else {
+            if (row_ok && nb < ep.N)
+              epilogue_chunk(ep, m, nb, v, bs + col0 + c * 32, best_v, best_i);
+          }
         }
         tc_fence_before();
         __syncwarp();
@@ -791,19 +835,20 @@ int num_sms() {
 // MINB = 2: two co-resident CTAs per SM (half-depth stage ring, <= 96
 // registers) for the skinny decoder GEMMs, so a second tile (or another
 // decode lane's kernel) hides the TMA / MMA / epilogue latency of the first.
-template <int BN, int STAGES, int TOPK = 0, bool I8 = false, int MINB = 1>
+template <int BN, int STAGES, int TOPK = 0, bool I8 = false, int MINB = 1, bool STG = false>
 cudaError_t launch_tc(const CUtensorMap& ta, const CUtensorMap& tw, const GemmArgs& g,
                       const EpiParams& ep, cudaStream_t s) {
-  using Cfg = TcCfg<BN, STAGES, I8>;
+  using Cfg = TcCfg<BN, STAGES, I8, 0, 0, STG>;
   static_assert(Cfg::kSmem <= 227 * 1024, "GEMM stage ring exceeds shared memory");
   static_assert(MINB == 1 || MINB * (Cfg::kSmem + 1024) <= 228 * 1024, "MINB CTAs do not fit");
-  cudaError_t e = set_max_smem((const void*)gemm_tc_kernel<BN, STAGES, TOPK, I8, MINB>);
+  auto kern = gemm_tc_kernel<BN, STAGES, TOPK, I8, MINB, 0, 0, STG>;
+  cudaError_t e = set_max_smem((const void*)kern);
   if (e != cudaSuccess) return e;
   const int tiles_n = (g.N + BN - 1) / BN;
   const int tiles = tiles_n * ((g.M + kBM - 1) / kBM);
   const int grid = tiles < MINB * num_sms() ? tiles : MINB * num_sms();
   const uint32_t idesc = I8 ? umma_idesc_i8(kBM, BN) : umma_idesc_f16(kBM, BN, g.in_dtype == kBF16);
-  return launch_k(gemm_tc_kernel<BN, STAGES, TOPK, I8, MINB>, dim3(grid), dim3(kTcThreads),
+  return launch_k(kern, dim3(grid), dim3(kTcThreads),
                   (size_t)Cfg::kSmem, s, ta, tw, I8 ? g.Kp : g.K, idesc, ep, tiles_n, tiles);
 }
 
@@ -880,6 +925,15 @@ int gemm_tile_n() { return kWBox; }
 // Opt-in (FNMT_GEMM_AST=1): r01 measured the A-stationary vocab GEMM (BN 128, 5 W stages)
 // at 688 TFLOP/s vs 1035 for the streamed BN 256 kernel — 33% fewer L2 bytes per FLOP, but
 // five 16 KB stages hold only ~0.45 us of MMA work, less than the TMA latency.
+bool staged_store_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("FNMT_GEMM_STG");
+    on = !(e && e[0] == '0');
+  }
+  return on != 0;
+}
+
 bool ast_enabled() {
   static int on = -1;
   if (on < 0) {
@@ -1020,11 +1074,17 @@ cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t s) {
     return g.topk.K == 4 ? launch_tc<256, 4, 4>(*pa, *pw, g, ep, s)
                          : launch_tc<256, 4, 8>(*pa, *pw, g, ep, s);
   }
+  const bool stg = g.epi == kEpiStore && !g.resid && staged_store_enabled();
   switch (pick_bn(g.M, g.N)) {
-    case 256: return launch_tc<256, 4>(*pa, *pw, g, ep, s);
-    case 128: return launch_tc<128, 6>(*pa, *pw, g, ep, s);
+    case 256:
+      if (stg) return launch_tc<256, 3, 0, false, 1, true>(*pa, *pw, g, ep, s);
+      return launch_tc<256, 4>(*pa, *pw, g, ep, s);
+    case 128:
+      if (stg) return launch_tc<128, 5, 0, false, 1, true>(*pa, *pw, g, ep, s);
+      return launch_tc<128, 6>(*pa, *pw, g, ep, s);
     default:
       if (g.K <= 1024 && dual_cta_enabled()) return launch_tc<64, 4, 0, false, 2>(*pa, *pw, g, ep, s);
+      if (stg) return launch_tc<64, 7, 0, false, 1, true>(*pa, *pw, g, ep, s);
       return launch_tc<64, 8>(*pa, *pw, g, ep, s);
   }
 }

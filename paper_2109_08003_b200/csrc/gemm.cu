@@ -925,11 +925,14 @@ int gemm_tile_n() { return kWBox; }
 // Opt-in (FNMT_GEMM_AST=1): r01 measured the A-stationary vocab GEMM (BN 128, 5 W stages)
 // at 688 TFLOP/s vs 1035 for the streamed BN 256 kernel — 33% fewer L2 bytes per FLOP, but
 // five 16 KB stages hold only ~0.45 us of MMA work, less than the TMA latency.
+// Opt-in (FNMT_GEMM_STG=1): r01 measured no gain in decode (785 vs 789 us per 9216-row step)
+// and slower encoder GEMMs (26.4 vs 20.6 ms per 16k sentences: the staging square costs a
+// pipeline stage) — L2 absorbs the row-per-thread 16-byte stores.
 bool staged_store_enabled() {
   static int on = -1;
   if (on < 0) {
     const char* e = getenv("FNMT_GEMM_STG");
-    on = !(e && e[0] == '0');
+    on = e && e[0] == '1';
   }
   return on != 0;
 }
@@ -1015,12 +1018,19 @@ bool make_tmap_kv(CUtensorMap* out, const void* base, int dtype, int64_t rows, i
   return true;
 }
 
-// N tile: the largest of 256/128/64 that still gives about one wave of tiles.
+// N tile: the largest of 256/128/64 that still gives about one wave of tiles
+// (>= FNMT_BN_WAVE x SMs tiles, default 1.0).
 int pick_bn(int M, int N) {
+  static double wave = -1.0;
+  if (wave < 0) {
+    const char* e = getenv("FNMT_BN_WAVE");
+    wave = e ? atof(e) : 1.0;
+    if (!(wave > 0.1 && wave < 4.0)) wave = 1.0;
+  }
   const int mt = (M + kBM - 1) / kBM;
-  const int sms = num_sms();
+  const double need = wave * num_sms();
   for (int bn : {256, 128}) {
-    if ((int64_t)mt * ((N + bn - 1) / bn) >= sms) return bn;
+    if ((double)mt * ((N + bn - 1) / bn) >= need) return bn;
   }
   return 64;
 }

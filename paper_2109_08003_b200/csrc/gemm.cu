@@ -1018,14 +1018,15 @@ bool make_tmap_kv(CUtensorMap* out, const void* base, int dtype, int64_t rows, i
   return true;
 }
 
-// N tile: the largest of 256/128/64 that still gives about one wave of tiles
-// (>= FNMT_BN_WAVE x SMs tiles, default 1.0).
+// N tile: the largest of 256/128/64 that still gives >= FNMT_BN_WAVE x SMs
+// tiles (default 0.6: r01 A/B at 9216-row decode steps 740 / 757 / 768 / 798 us
+// for 0.6 / 0.9 / 1.0 / 2.0 — bigger N tiles re-read A less often).
 int pick_bn(int M, int N) {
   static double wave = -1.0;
   if (wave < 0) {
     const char* e = getenv("FNMT_BN_WAVE");
-    wave = e ? atof(e) : 1.0;
-    if (!(wave > 0.1 && wave < 4.0)) wave = 1.0;
+    wave = e ? atof(e) : 0.6;
+    if (!(wave > 0.1 && wave < 4.0)) wave = 0.6;
   }
   const int mt = (M + kBM - 1) / kBM;
   const double need = wave * num_sms();

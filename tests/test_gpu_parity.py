@@ -209,3 +209,20 @@ def test_multihead_decode_rows_fp16(d, heads, dec):
     got = split_off(out, olen, off)
     want = O.beam(a, p, tok, valid, 4)
     assert sum(x == y for x, y in zip(got, want)) >= len(rows) - 2
+
+
+@pytest.mark.parametrize("tag", ["tiny", "d32_student", "d64_h8_dec6", "d64_h1_l1"])
+def test_bf16_logits_within_tolerance(golden, tag):
+    """bf16 storage (the Deep-12-768 configuration's dtype): logits of forced
+    decode steps within 2e-2 relative of the reference (bf16 keeps 8 mantissa
+    bits vs fp16's 11, so the fp16 bound of 1e-2 is doubled)."""
+    cfg, w, get = case(golden, tag)
+    m = GpuTranslationModel(cfg, w, dtype="bf16")
+    tok, valid = get("tokens"), get("valid")
+    enc = m.encode(tok, valid)
+    assert rel_err(enc.states, get("states")) <= 2e-2
+    cache = m.init_cache(enc)
+    prev = np.full(tok.shape[0], 2, np.int64)
+    for t in range(6):
+        assert rel_err(m.step(cache, prev), get("logits")[t]) <= 2e-2, t
+        prev = get("forced")[:, t]

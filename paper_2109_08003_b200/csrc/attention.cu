@@ -404,178 +404,6 @@ __global__ void __launch_bounds__(NT) attn_decode_kernel(DecAttnArgs a, float qs
 }
 
 
-// Single-pass decode attention with an online softmax (fp16 / bf16 storage).
-// Slot = (warp, lane group of G lanes); slot s walks keys s, s + SLOTS, ...
-// loading each key's K and V chunks together (U keys in flight per slot) and
-// keeps a running (max m, sum l, output o) — o rescaled by exp(m_old - m_new)
-// when the max grows.  The slots merge in a fixed order at the end:
-//   out = sum_s o_s e^(m_s - M) / sum_s l_s e^(m_s - M).
-// Mathematically the reference's max-shifted softmax followed by the value
-// product (tensor.py:70-81, model.py:226-240); the rounding differs only by
-// where the 1/sum is applied, far inside the fp16 tolerance.  One pass over
-// K and V instead of score / softmax / value phases separated by barriers.
-// RQ > 1 (cross attention of a beam: the k rows of a sentence read the same
-// encoder keys): the CTA takes the RQ query rows of one sentence and loads
-// every key / value once for all of them.
-template <typename T, int G, int CH, int NT, int U, int RQ = 1>
-__global__ void __launch_bounds__(NT) attn_decode_online_kernel(DecAttnArgs a, float qscale) {
-  pdl_trigger();
-  pdl_wait();
-  constexpr int VEC = Vec16<T>::N;
-  constexpr int KPW = 32 / G;
-  constexpr int SLOTS = (NT / 32) * KPW;
-  extern __shared__ float sm[];
-  const int dk = a.dk;
-  float* qs = sm;                          // [RQ][dk]
-  float* so = qs + RQ * dk;                // [SLOTS][RQ][dk]
-  float* sml = so + SLOTS * RQ * dk;       // [SLOTS][RQ][2]
-  const int r0 = blockIdx.x * RQ, h = blockIdx.y;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const DecCtx c = decode_setup<T>(a, r0, h);   // RQ > 1: cross mode, one sentence
-  for (int e = tid; e < RQ * dk; e += NT) {
-    const int rq = e / dk, ee = e - rq * dk;
-    qs[e] = to_f32(reinterpret_cast<const T*>(a.q)[(size_t)(r0 + rq) * a.ldq + h * dk + ee]) * qscale;
-  }
-  __syncthreads();
-
-  const T* kb = reinterpret_cast<const T*>(a.k) + h * dk;
-  const T* vb = reinterpret_cast<const T*>(a.v) + h * dk;
-  const int g = lane / G, li = lane % G;
-  const int slot = warp * KPW + g;
-  float m[RQ], l[RQ];
-  float o[RQ][CH][VEC];
-#pragma unroll
-  for (int rq = 0; rq < RQ; ++rq) {
-    m[rq] = -INFINITY;
-    l[rq] = 0.f;
-#pragma unroll
-    for (int ch = 0; ch < CH; ++ch)
-#pragma unroll
-      for (int i = 0; i < VEC; ++i) o[rq][ch][i] = 0.f;
-  }
-
-  // the loop bound is warp-uniform (lane groups of one warp may have different
-  // key counts left; the group reductions below shuffle across the full warp)
-  for (int jw = warp * KPW; jw < c.nk; jw += SLOTS * U) {
-    const int j0 = jw + g;
-    uint4 rk[U][CH], rv[U][CH];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int j = j0 + u * SLOTS;
-      if (j < c.nk) {
-        const int64_t row = decode_key_row(a, c, r0, j);
-        const T* kr = kb + row * a.ldkv;
-        const T* vr = vb + row * a.ldkv;
-#pragma unroll
-        for (int ch = 0; ch < CH; ++ch) {
-          const int e0 = (li + ch * G) * VEC;
-          if (e0 < dk) {
-            rk[u][ch] = *reinterpret_cast<const uint4*>(kr + e0);
-            rv[u][ch] = *reinterpret_cast<const uint4*>(vr + e0);
-          }
-        }
-      }
-    }
-    float sc[U][RQ];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int j = j0 + u * SLOTS;
-      float sacc[RQ];
-#pragma unroll
-      for (int rq = 0; rq < RQ; ++rq) sacc[rq] = 0.f;
-      if (j < c.nk) {
-#pragma unroll
-        for (int ch = 0; ch < CH; ++ch) {
-          const int e0 = (li + ch * G) * VEC;
-          if (e0 < dk) {
-            float f[VEC];
-            cvt16<T>(rk[u][ch], f);
-#pragma unroll
-            for (int rq = 0; rq < RQ; ++rq)
-#pragma unroll
-              for (int i = 0; i < VEC; ++i) sacc[rq] = fmaf(qs[rq * dk + e0 + i], f[i], sacc[rq]);
-          }
-        }
-      }
-#pragma unroll
-      for (int rq = 0; rq < RQ; ++rq) {
-#pragma unroll
-        for (int off = G / 2; off > 0; off >>= 1)
-          sacc[rq] += __shfl_xor_sync(0xffffffffu, sacc[rq], off);
-        sc[u][rq] = j < c.nk ? (c.all_masked ? sacc[rq] + kMaskValue : sacc[rq]) : -INFINITY;
-      }
-    }
-#pragma unroll
-    for (int rq = 0; rq < RQ; ++rq) {
-      float mx = m[rq];
-#pragma unroll
-      for (int u = 0; u < U; ++u) mx = fmaxf(mx, sc[u][rq]);
-      if (mx == -INFINITY) continue;   // no live key in this round for this slot
-      const float resc = expf(m[rq] - mx);   // m = -inf on the first live round -> 0
-      l[rq] *= resc;
-#pragma unroll
-      for (int ch = 0; ch < CH; ++ch)
-#pragma unroll
-        for (int i = 0; i < VEC; ++i) o[rq][ch][i] *= resc;
-      m[rq] = mx;
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int j = j0 + u * SLOTS;
-      if (j < c.nk) {
-        float p[RQ];
-#pragma unroll
-        for (int rq = 0; rq < RQ; ++rq) {
-          p[rq] = expf(sc[u][rq] - m[rq]);
-          l[rq] += p[rq];
-        }
-#pragma unroll
-        for (int ch = 0; ch < CH; ++ch) {
-          const int e0 = (li + ch * G) * VEC;
-          if (e0 < dk) {
-            float f[VEC];
-            cvt16<T>(rv[u][ch], f);
-#pragma unroll
-            for (int rq = 0; rq < RQ; ++rq)
-#pragma unroll
-              for (int i = 0; i < VEC; ++i) o[rq][ch][i] = fmaf(p[rq], f[i], o[rq][ch][i]);
-          }
-        }
-      }
-    }
-  }
-#pragma unroll
-  for (int rq = 0; rq < RQ; ++rq) {
-#pragma unroll
-    for (int ch = 0; ch < CH; ++ch) {
-      const int e0 = (li + ch * G) * VEC;
-      if (e0 < dk)
-#pragma unroll
-        for (int i = 0; i < VEC; ++i) so[(slot * RQ + rq) * dk + e0 + i] = o[rq][ch][i];
-    }
-    if (li == 0) {
-      sml[2 * (slot * RQ + rq)] = m[rq];
-      sml[2 * (slot * RQ + rq) + 1] = l[rq];
-    }
-  }
-  __syncthreads();
-  for (int e = tid; e < RQ * dk; e += NT) {
-    const int rq = e / dk, ee = e - rq * dk;
-    float M = -INFINITY;
-    for (int s2 = 0; s2 < SLOTS; ++s2) M = fmaxf(M, sml[2 * (s2 * RQ + rq)]);
-    float L = 0.f, O = 0.f;
-    for (int s2 = 0; s2 < SLOTS; ++s2) {
-      const float ms = sml[2 * (s2 * RQ + rq)];
-      if (ms == -INFINITY) continue;
-      const float w = expf(ms - M);
-      L = fmaf(sml[2 * (s2 * RQ + rq) + 1], w, L);
-      O = fmaf(so[(s2 * RQ + rq) * dk + ee], w, O);
-    }
-    reinterpret_cast<T*>(a.out)[(size_t)(r0 + rq) * a.ldo + h * dk + ee] = from_f32<T>(O / L);
-  }
-}
-
-
 // Multi-head decode attention, one CTA per ROW covering all H heads.  A key
 // row of all heads is d contiguous elements (H x dk), so a warp streams it
 // exactly like the single-head dk = d case (G = 32 lanes, CH 16-byte chunks per
@@ -960,48 +788,8 @@ cudaError_t launch_dec_async(const DecAttnArgs& a, float qscale, cudaStream_t s)
                   a, qscale);
 }
 
-// Opt-in (FNMT_DEC_ONLINE=1): r01 measured the single-pass kernel slower than the two-pass
-// one — 6-1-1 6.71M vs 6.77M, 6-1-8 5.26M vs 5.64M, 6-6-8 beam 4 0.407M vs 0.439M words/s
-// (attn_dec 39 / 66 / 1270 ms vs 38 / 53 / 1130 ms): the per-key exp / rescale work sits on
-// the load critical path, where the two-pass kernel's value phase spreads keys over all
-// threads.
-bool dec_online_enabled() {
-  static int on = -1;
-  if (on < 0) {
-    const char* e = getenv("FNMT_DEC_ONLINE");
-    on = e && e[0] == '1';
-  }
-  return on != 0;
-}
-
-template <typename T, int G, int CH, int RQ>
-cudaError_t launch_dec_online_rq(const DecAttnArgs& a, float qscale, cudaStream_t s) {
-  constexpr int NT = 128;
-  constexpr int U = G == 32 ? 2 : 4;
-  constexpr int SLOTS = (NT / 32) * (32 / G);
-  auto kern = attn_decode_online_kernel<T, G, CH, NT, U, RQ>;
-  const size_t smem = sizeof(float) * ((size_t)a.dk * RQ * (SLOTS + 1) + 2 * SLOTS * RQ);
-  if (smem > 227 * 1024) return cudaErrorInvalidValue;
-  if (smem > 48 * 1024) {
-    cudaError_t e = set_max_smem((const void*)kern);
-    if (e != cudaSuccess) return e;
-  }
-  return launch_k(kern, dim3(a.rows / RQ, a.heads), dim3(NT), smem, s, a, qscale);
-}
-
-template <typename T, int G, int CH>
-cudaError_t launch_dec_online(const DecAttnArgs& a, float qscale, cudaStream_t s) {
-  // beam cross attention: the rows of one sentence share its encoder keys
-  if (!a.self_mode && a.rows_per_seq == 4 && a.rows % 4 == 0)
-    return launch_dec_online_rq<T, G, CH, 4>(a, qscale, s);
-  return launch_dec_online_rq<T, G, CH, 1>(a, qscale, s);
-}
-
 template <typename T, int G, int CH>
 cudaError_t launch_dec(const DecAttnArgs& a, float qscale, cudaStream_t s) {
-  if constexpr (!std::is_same<T, float>::value) {
-    if (dec_online_enabled()) return launch_dec_online<T, G, CH>(a, qscale, s);
-  }
   // few (row, head) blocks -> wide blocks so the SMs still have enough warps in flight
   // cp.async staging measured faster for 8 heads (dk=64) only (r01: 6-1-8 3.92M vs 3.67M
   // words/s; 6-1-1 3.92M vs 4.32M)

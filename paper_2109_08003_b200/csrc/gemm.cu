@@ -38,7 +38,6 @@ constexpr int kBM = 128;
 constexpr int kBK = 64;
 constexpr int kWBox = 64;   // W TMA box rows; BN/64 boxes per stage
 constexpr int kABytes = kBM * kBK * 2;
-constexpr int kEpiWarpsC = 8;   // epilogue warps (kEpiWarps, needed before its definition)
 
 struct EpiParams {
   const float* bias;
@@ -239,39 +238,6 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& ep, int m, int n
   }
 }
 
-// kEpiStore without residual, coalesced: the warp's 32 rows x 32 columns go
-// through a padded smem square so each store instruction writes 32
-// consecutive columns of ONE row (a 128-byte f32 / 64-byte 16-bit line)
-// instead of 32 rows' 16-byte pieces.  Same values as epilogue_chunk.
-__device__ __forceinline__ void staged_store_chunk(const EpiParams& ep, int row0, int nb,
-                                                   const float (&v)[32], const float* bs,
-                                                   float* sq, int lane) {
-#pragma unroll
-  for (int i = 0; i < 32; ++i) {
-    float x = v[i] + bs[i];
-    if (ep.relu) x = fmaxf(x, 0.f);
-    sq[lane * 33 + i] = x;
-  }
-  __syncwarp();
-  const int n = nb + lane;
-  const bool col_ok = n < ep.N;
-#pragma unroll 4
-  for (int rr = 0; rr < 32; ++rr) {
-    const int m = row0 + rr;
-    const float x = sq[rr * 33 + lane];
-    if (m < ep.M && col_ok) {
-      const size_t off = (size_t)m * ep.ldc + n;
-      if (ep.c_dtype == kF32)
-        reinterpret_cast<float*>(ep.C)[off] = x;
-      else if (ep.c_dtype == kF16)
-        reinterpret_cast<__half*>(ep.C)[off] = __float2half_rn(x);
-      else
-        reinterpret_cast<__nv_bfloat16*>(ep.C)[off] = __float2bfloat16_rn(x);
-    }
-  }
-  __syncwarp();
-}
-
 // int8 epilogue: turn 32 s32 accumulators of row m into the f32 value of
 // quant8.qgemm (quant8.py:246-278) — the zeropoint cross terms expanded
 // against the row / column sums, evaluated in double in the reference's
@@ -412,34 +378,24 @@ __device__ __forceinline__ void norm_epilogue(const EpiParams& ep, uint32_t tadd
 // persistent tcgen05 kernel
 
 // Every stage row is 128 bytes of K: 64 fp16/bf16 elements, or 128 int8.
-template <int BN, int STAGES, bool I8 = false, int CN = 0, int KA = 0, bool STG = false>
+template <int BN, int STAGES, bool I8 = false, int CN = 0>
 struct TcCfg {
-  // STG: per epilogue warp a 32 x 33 fp32 staging square for coalesced stores
-  static constexpr int kStgBytes = STG ? kEpiWarpsC * 32 * 33 * 4 : 0;
   static constexpr int kBKe = I8 ? 2 * kBK : kBK;   // K elements per stage
   static constexpr int kBBytes = BN * kBK * 2;
-  // KA > 0 (A-stationary): the CTA's 128-row A block (KA k-blocks) stays in
-  // smem while it walks N tiles; the stage ring carries only W tiles.
-  static constexpr int kARegion = KA ? KA * kABytes : 0;
-  static constexpr int kStage = (KA ? 0 : kABytes) + kBBytes;
+  static constexpr int kStage = kABytes + kBBytes;
   static constexpr int kTmemCols = 2 * BN;   // double-buffered accumulator
   static constexpr int kColBytes = I8 ? 16 : 4;   // bias (+ scale, zeropoint, column sum)
   // kEpiNorm: row-statistic slots [parity][pass][rank][128] + half-row partials [2][128]
   static constexpr int kNormBytes = CN ? (4 * CN * kBM + 2 * kBM) * 8 + 64 : 0;
-  static constexpr int kSmem =
-      1024 + kARegion + STAGES * kStage + 2 * BN * kColBytes + kNormBytes + kStgBytes + 256;
+  static constexpr int kSmem = 1024 + STAGES * kStage + 2 * BN * kColBytes + kNormBytes + 256;
 };
 
 // Tile of this CTA's it-th iteration (-1 when done).  Plain: a grid-stride
 // walk.  Clustered (CN > 0, kEpiNorm): the CN CTAs of a cluster take the CN
 // N tiles of the same 128-row block, block after block.
-template <int CN, bool AST = false>
+template <int CN>
 __device__ __forceinline__ int tile_at(int it, int tiles, int tiles_n) {
-  if constexpr (AST) {   // a contiguous, m-major range of tiles per CTA
-    const int b = (int)((int64_t)blockIdx.x * tiles / gridDim.x);
-    const int e = (int)((int64_t)(blockIdx.x + 1) * tiles / gridDim.x);
-    return b + it < e ? b + it : -1;
-  } else if constexpr (CN == 0) {
+  if constexpr (CN == 0) {
     const int t = blockIdx.x + it * gridDim.x;
     return t < tiles ? t : -1;
   } else {
@@ -520,18 +476,16 @@ __device__ __forceinline__ void topk_epilogue(const EpiParams& ep, uint32_t tadd
   }
 }
 
-template <int BN, int STAGES, int TOPK, bool I8 = false, int MINB = 1, int CN = 0, int KA = 0,
-          bool STG = false>
+template <int BN, int STAGES, int TOPK, bool I8 = false, int MINB = 1, int CN = 0>
 __global__ void __launch_bounds__(kTcThreads, MINB)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmw,
                    int K, uint32_t idesc, EpiParams ep, int tiles_n, int tiles) {
-  using Cfg = TcCfg<BN, STAGES, I8, CN, KA, STG>;
-  constexpr bool AST = KA > 0;
+  using Cfg = TcCfg<BN, STAGES, I8, CN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
   uint8_t* sA = base;
-  uint8_t* sB = base + (AST ? KA : STAGES) * kABytes;
+  uint8_t* sB = base + STAGES * kABytes;
   float* bias_s = reinterpret_cast<float*>(sB + STAGES * Cfg::kBBytes);   // [2][BN]
   // int8: [2][BN] column scale, zeropoint, column sum after the bias
   float* qsc_s = bias_s + 2 * BN;
@@ -541,14 +495,11 @@ __global__ void __launch_bounds__(kTcThreads, MINB)
   double* nslot = reinterpret_cast<double*>(bias_s + (Cfg::kColBytes / 4) * 2 * BN);
   double* nhalf = nslot + (CN ? 4 * CN * kBM : 0);
   uint64_t* nbar = reinterpret_cast<uint64_t*>(nhalf + (CN ? 2 * kBM : 0));   // [parity][pass]
-  float* stg = reinterpret_cast<float*>(nbar + (CN ? 4 : 0));   // STG: [kEpiWarps][32][33]
-  uint64_t* full = reinterpret_cast<uint64_t*>(stg + (STG ? kEpiWarpsC * 32 * 33 : 0));
+  uint64_t* full = nbar + (CN ? 4 : 0);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint64_t* afull = tempty + 2;     // A-stationary: A block landed / released
-  uint64_t* aempty = afull + 1;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(aempty + 1);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -567,8 +518,6 @@ __global__ void __launch_bounds__(kTcThreads, MINB)
     }
     if constexpr (CN > 0)
       for (int b = 0; b < 4; ++b) mbar_init(nbar + b, CN);
-    mbar_init(afull, 1);
-    mbar_init(aempty, 1);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc(tslot, Cfg::kTmemCols);
@@ -586,29 +535,15 @@ __global__ void __launch_bounds__(kTcThreads, MINB)
     if (lane == 0) {
       int s = 0;
       uint32_t ph = 0;
-      int cur_mb = -1;
-      uint32_t aeph = 0;
       for (int it = 0;; ++it) {
-        const int tile = tile_at<CN, AST>(it, tiles, tiles_n);
+        const int tile = tile_at<CN>(it, tiles, tiles_n);
         if (tile < 0) break;
         const int m0 = (tile / tiles_n) * kBM;
         const int n0 = (tile % tiles_n) * BN;
-        if constexpr (AST) {
-          if (tile / tiles_n != cur_mb) {   // (re)load the resident A block
-            if (cur_mb >= 0) {
-              mbar_wait(aempty, aeph);
-              aeph ^= 1;
-            }
-            mbar_expect_tx(afull, nk * kABytes);
-            for (int kb = 0; kb < nk; ++kb)
-              tma_load_2d(sA + kb * kABytes, &tma, afull, kb * Cfg::kBKe, m0);
-            cur_mb = tile / tiles_n;
-          }
-        }
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(empty + s, ph ^ 1);
           mbar_expect_tx(full + s, Cfg::kStage);
-          if constexpr (!AST) tma_load_2d(sA + s * kABytes, &tma, full + s, kb * Cfg::kBKe, m0);
+          tma_load_2d(sA + s * kABytes, &tma, full + s, kb * Cfg::kBKe, m0);
 #pragma unroll
           for (int j = 0; j < BN / kWBox; ++j)
             tma_load_2d(sB + s * Cfg::kBBytes + j * kWBox * 128, &tmw, full + s, kb * Cfg::kBKe,
@@ -626,25 +561,15 @@ __global__ void __launch_bounds__(kTcThreads, MINB)
       uint32_t ph = 0;
       int acc = 0;
       uint32_t aph = 0;
-      int cur_mb = -1;
-      uint32_t afph = 0;
       for (int it = 0;; ++it) {
-        const int tile = tile_at<CN, AST>(it, tiles, tiles_n);
-        if (tile < 0) break;
-        if constexpr (AST) {
-          if (tile / tiles_n != cur_mb) {
-            mbar_wait(afull, afph);
-            afph ^= 1;
-            cur_mb = tile / tiles_n;
-          }
-        }
+        if (tile_at<CN>(it, tiles, tiles_n) < 0) break;
         mbar_wait(tempty + acc, aph ^ 1);
         tc_fence_after();
         const uint32_t d = tmem + acc * BN;
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(full + s, ph);
           tc_fence_after();
-          const uint64_t ad = umma_desc_sw128(smem_u32(sA + (AST ? kb : s) * kABytes));
+          const uint64_t ad = umma_desc_sw128(smem_u32(sA + s * kABytes));
           const uint64_t bd = umma_desc_sw128(smem_u32(sB + s * Cfg::kBBytes));
           // 4 MMAs of 32 bytes of K each (K = 16 fp16 or K = 32 int8)
 #pragma unroll
@@ -661,10 +586,6 @@ __global__ void __launch_bounds__(kTcThreads, MINB)
           }
         }
         tc_commit(tfull + acc);
-        if constexpr (AST) {   // last tile of this A block: let the producer overwrite it
-          const int nxt = tile_at<CN, AST>(it + 1, tiles, tiles_n);
-          if (nxt < 0 || nxt / tiles_n != cur_mb) tc_commit(aempty);
-        }
         acc ^= 1;
         if (acc == 0) aph ^= 1;
       }
@@ -677,7 +598,7 @@ __global__ void __launch_bounds__(kTcThreads, MINB)
     int acc = 0;
     uint32_t aph = 0;
     for (int it = 0;; ++it) {
-      const int tile = tile_at<CN, AST>(it, tiles, tiles_n);
+      const int tile = tile_at<CN>(it, tiles, tiles_n);
       if (tile < 0) break;
       const int m0 = (tile / tiles_n) * kBM;
       const int n0 = (tile % tiles_n) * BN;
@@ -724,14 +645,8 @@ __global__ void __launch_bounds__(kTcThreads, MINB)
               q_dequant_chunk(ep, m, v, qsc_s + o, qzp_s + o, qcs_s + o);
             }
           }
-          if constexpr (STG) {
-            if (nb < ep.N)   // warp-uniform
-              staged_store_chunk(ep, m0 + quarter * 32, nb, v, bs + col0 + c * 32,
-                                 stg + (warp - 2) * 32 * 33, lane);
-          } else {
-            if (row_ok && nb < ep.N)
-              epilogue_chunk(ep, m, nb, v, bs + col0 + c * 32, best_v, best_i);
-          }
+          if (row_ok && nb < ep.N)
+            epilogue_chunk(ep, m, nb, v, bs + col0 + c * 32, best_v, best_i);
         }
         tc_fence_before();
         __syncwarp();
@@ -835,13 +750,13 @@ int num_sms() {
 // MINB = 2: two co-resident CTAs per SM (half-depth stage ring, <= 96
 // registers) for the skinny decoder GEMMs, so a second tile (or another
 // decode lane's kernel) hides the TMA / MMA / epilogue latency of the first.
-template <int BN, int STAGES, int TOPK = 0, bool I8 = false, int MINB = 1, bool STG = false>
+template <int BN, int STAGES, int TOPK = 0, bool I8 = false, int MINB = 1>
 cudaError_t launch_tc(const CUtensorMap& ta, const CUtensorMap& tw, const GemmArgs& g,
                       const EpiParams& ep, cudaStream_t s) {
-  using Cfg = TcCfg<BN, STAGES, I8, 0, 0, STG>;
+  using Cfg = TcCfg<BN, STAGES, I8>;
   static_assert(Cfg::kSmem <= 227 * 1024, "GEMM stage ring exceeds shared memory");
   static_assert(MINB == 1 || MINB * (Cfg::kSmem + 1024) <= 228 * 1024, "MINB CTAs do not fit");
-  auto kern = gemm_tc_kernel<BN, STAGES, TOPK, I8, MINB, 0, 0, STG>;
+  auto kern = gemm_tc_kernel<BN, STAGES, TOPK, I8, MINB>;
   cudaError_t e = set_max_smem((const void*)kern);
   if (e != cudaSuccess) return e;
   const int tiles_n = (g.N + BN - 1) / BN;
@@ -850,23 +765,6 @@ cudaError_t launch_tc(const CUtensorMap& ta, const CUtensorMap& tw, const GemmAr
   const uint32_t idesc = I8 ? umma_idesc_i8(kBM, BN) : umma_idesc_f16(kBM, BN, g.in_dtype == kBF16);
   return launch_k(kern, dim3(grid), dim3(kTcThreads),
                   (size_t)Cfg::kSmem, s, ta, tw, I8 ? g.Kp : g.K, idesc, ep, tiles_n, tiles);
-}
-
-// A-stationary vocab projection (KA resident A k-blocks, K = 64 KA exactly).
-template <int BN, int STAGES, int KA>
-cudaError_t launch_tc_ast(const CUtensorMap& ta, const CUtensorMap& tw, const GemmArgs& g,
-                          const EpiParams& ep, cudaStream_t s) {
-  using Cfg = TcCfg<BN, STAGES, false, 0, KA>;
-  static_assert(Cfg::kSmem <= 227 * 1024, "A-stationary GEMM exceeds shared memory");
-  auto kern = gemm_tc_kernel<BN, STAGES, 0, false, 1, 0, KA>;
-  cudaError_t e = set_max_smem((const void*)kern);
-  if (e != cudaSuccess) return e;
-  const int tiles_n = (g.N + BN - 1) / BN;
-  const int tiles = tiles_n * ((g.M + kBM - 1) / kBM);
-  const int grid = tiles < num_sms() ? tiles : num_sms();
-  const uint32_t idesc = umma_idesc_f16(kBM, BN, g.in_dtype == kBF16);
-  return launch_k(kern, dim3(grid), dim3(kTcThreads), (size_t)Cfg::kSmem, s, ta, tw, g.K, idesc,
-                  ep, tiles_n, tiles);
 }
 
 // kEpiNorm: clusters of CN CTAs along N (one per N tile of a row block).
@@ -921,30 +819,6 @@ bool gemm_norm_supported(int N, int in_dtype) {
 }
 
 int gemm_tile_n() { return kWBox; }
-
-// Opt-in (FNMT_GEMM_AST=1): r01 measured the A-stationary vocab GEMM (BN 128, 5 W stages)
-// at 688 TFLOP/s vs 1035 for the streamed BN 256 kernel — 33% fewer L2 bytes per FLOP, but
-// five 16 KB stages hold only ~0.45 us of MMA work, less than the TMA latency.
-// Opt-in (FNMT_GEMM_STG=1): r01 measured no gain in decode (785 vs 789 us per 9216-row step)
-// and slower encoder GEMMs (26.4 vs 20.6 ms per 16k sentences: the staging square costs a
-// pipeline stage) — L2 absorbs the row-per-thread 16-byte stores.
-bool staged_store_enabled() {
-  static int on = -1;
-  if (on < 0) {
-    const char* e = getenv("FNMT_GEMM_STG");
-    on = e && e[0] == '1';
-  }
-  return on != 0;
-}
-
-bool ast_enabled() {
-  static int on = -1;
-  if (on < 0) {
-    const char* e = getenv("FNMT_GEMM_AST");
-    on = e && e[0] == '1';
-  }
-  return on != 0;
-}
 
 bool dual_cta_enabled() {
   static int on = -1;
@@ -1078,24 +952,16 @@ cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t s) {
       default: return launch_tc_norm<128, 4, 8>(*pa, *pw, g, ep, s);
     }
   }
-  if (g.epi == kEpiArgmax && g.K == 512 && ast_enabled())
-    return launch_tc_ast<128, 5, 8>(*pa, *pw, g, ep, s);
   if (g.epi == kEpiTopK) {
     static_assert(kTopKTile == 128, "top-K partial tiles are half of BN = 256");
     return g.topk.K == 4 ? launch_tc<256, 4, 4>(*pa, *pw, g, ep, s)
                          : launch_tc<256, 4, 8>(*pa, *pw, g, ep, s);
   }
-  const bool stg = g.epi == kEpiStore && !g.resid && staged_store_enabled();
   switch (pick_bn(g.M, g.N)) {
-    case 256:
-      if (stg) return launch_tc<256, 3, 0, false, 1, true>(*pa, *pw, g, ep, s);
-      return launch_tc<256, 4>(*pa, *pw, g, ep, s);
-    case 128:
-      if (stg) return launch_tc<128, 5, 0, false, 1, true>(*pa, *pw, g, ep, s);
-      return launch_tc<128, 6>(*pa, *pw, g, ep, s);
+    case 256: return launch_tc<256, 4>(*pa, *pw, g, ep, s);
+    case 128: return launch_tc<128, 6>(*pa, *pw, g, ep, s);
     default:
       if (g.K <= 1024 && dual_cta_enabled()) return launch_tc<64, 4, 0, false, 2>(*pa, *pw, g, ep, s);
-      if (stg) return launch_tc<64, 7, 0, false, 1, true>(*pa, *pw, g, ep, s);
       return launch_tc<64, 8>(*pa, *pw, g, ep, s);
   }
 }

@@ -30,9 +30,7 @@ inline cudaError_t set_max_smem(const void* func) {
 // FNMT_PDL=0.  Kernels launched this way call pdl_wait() before touching
 // their predecessor's data (common.cuh).
 bool pdl_enabled();
-bool dual_cta_enabled();
-bool ast_enabled();
-bool staged_store_enabled();   // FNMT_GEMM_STG=0: row-per-thread epilogue stores        // FNMT_GEMM_AST=1 enables the A-stationary vocab GEMM   // FNMT_GEMM_DUAL=0 disables 2-CTA/SM decoder GEMMs
+bool dual_cta_enabled();   // FNMT_GEMM_DUAL=0 disables 2-CTA/SM decoder GEMMs
 template <typename... KArgs, typename... Args>
 cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                      Args&&... args) {

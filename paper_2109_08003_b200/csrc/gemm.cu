@@ -767,6 +767,194 @@ cudaError_t launch_tc(const CUtensorMap& ta, const CUtensorMap& tw, const GemmAr
                   (size_t)Cfg::kSmem, s, ta, tw, I8 ? g.Kp : g.K, idesc, ep, tiles_n, tiles);
 }
 
+
+// ---------------------------------------------------------------------------
+// CTA-pair kernel (cta_group::2): a 256 x BN tile per cluster of 2 CTAs.
+// Each CTA stages its own 128 rows of A and BN/2 rows of W^T per k-block
+// (TMA completions counted on the leader's barrier); the leader's single
+// thread issues tcgen05.mma.cta_group::2 (M = 256) which reads both CTAs'
+// smem and accumulates each CTA's 128 rows x BN in its own TMEM; commits are
+// multicast to both CTAs.  Per CTA and k-block: 16 KB of A + BN/2 x 128 B of
+// W for 2 x 128 x BN x 64 FLOP — a third less L2 traffic per FLOP than the
+// single-CTA 128 x BN tile.  Epilogues are the single-CTA ones.
+template <int BN, int STAGES>
+struct Tc2Cfg {
+  static constexpr int kBHalf = BN / 2;
+  static constexpr int kBBytes = kBHalf * kBK * 2;
+  static constexpr int kStage = kABytes + kBBytes;
+  static constexpr int kTmemCols = 2 * BN;
+  static constexpr int kSmem = 1024 + STAGES * kStage + 2 * BN * 4 + 256;
+};
+
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(kTcThreads, 1)
+    gemm_tc2_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmw,
+                    int K, uint32_t idesc, EpiParams ep, int tiles_n, int tiles) {
+  using Cfg = Tc2Cfg<BN, STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* sA = base;
+  uint8_t* sB = base + STAGES * kABytes;
+  float* bias_s = reinterpret_cast<float*>(sB + STAGES * Cfg::kBBytes);   // [2][BN]
+  uint64_t* full = reinterpret_cast<uint64_t*>(bias_s + 2 * BN);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int ncl = gridDim.x / 2, cid = blockIdx.x / 2;
+  const int nk = (K + kBK - 1) / kBK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tma);
+    tma_prefetch_desc(&tmw);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(tfull + b, 1);
+      mbar_init(tempty + b, 2 * kEpiWarps);   // both CTAs' epilogue warps release it
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc_pair(tslot, Cfg::kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();   // barriers of both CTAs initialised, TMEM of the pair allocated
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  pdl_trigger();
+  pdl_wait();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      for (int tile = cid; tile < tiles; tile += ncl) {
+        const int m0 = (tile / tiles_n) * 2 * kBM + rank * kBM;
+        const int n0 = (tile % tiles_n) * BN + rank * Cfg::kBHalf;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(empty + s, ph ^ 1);
+          if (leader) mbar_expect_tx(full + s, 2 * Cfg::kStage);
+          tma_load_2d_pair(sA + s * kABytes, &tma, full + s, kb * kBK, m0);
+#pragma unroll
+          for (int j = 0; j < Cfg::kBHalf / kWBox; ++j)
+            tma_load_2d_pair(sB + s * Cfg::kBBytes + j * kWBox * 128, &tmw, full + s, kb * kBK,
+                             n0 + j * kWBox);
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      int acc = 0;
+      uint32_t aph = 0;
+      for (int tile = cid; tile < tiles; tile += ncl) {
+        mbar_wait(tempty + acc, aph ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + acc * BN;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(full + s, ph);
+          tc_fence_after();
+          const uint64_t ad = umma_desc_sw128(smem_u32(sA + s * kABytes));
+          const uint64_t bd = umma_desc_sw128(smem_u32(sB + s * Cfg::kBBytes));
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            tc_mma_f16_pair(d, ad + 2 * kk, bd + 2 * kk, idesc, (kb | kk) != 0 ? 1u : 0u);
+          tc_commit_pair(empty + s);
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+        tc_commit_pair(tfull + acc);
+        acc ^= 1;
+        if (acc == 0) aph ^= 1;
+      }
+    }
+  } else {
+    const int quarter = warp & 3;
+    const int half = (warp - 2) >> 2;
+    const uint32_t tempty_leader0 = mapa_shared(smem_u32(tempty), 0);
+    int acc = 0;
+    uint32_t aph = 0;
+    for (int tile = cid; tile < tiles; tile += ncl) {
+      const int m0 = (tile / tiles_n) * 2 * kBM + rank * kBM;
+      const int n0 = (tile % tiles_n) * BN;
+      float* bs = bias_s + acc * BN;
+      for (int i = threadIdx.x - 64; i < BN; i += kEpiWarps * 32)
+        bs[i] = (ep.bias && n0 + i < ep.N) ? ep.bias[n0 + i] : 0.f;
+      named_bar_sync(1, kEpiWarps * 32);
+      mbar_wait(tfull + acc, aph);
+      tc_fence_after();
+      const int m = m0 + quarter * 32 + lane;
+      const bool row_ok = m < ep.M;
+      const int col0 = half * (BN / 2);
+      const uint32_t taddr = tmem + acc * BN + col0 + ((uint32_t)(quarter * 32) << 16);
+      float best_v = -INFINITY;
+      int best_i = -1;
+#pragma unroll 1
+      for (int c = 0; c < BN / 64; ++c) {
+        float v[32];
+        tmem_ld32(taddr + c * 32, v);
+        const int nb = n0 + col0 + c * 32;
+        if (row_ok && nb < ep.N) epilogue_chunk(ep, m, nb, v, bs + col0 + c * 32, best_v, best_i);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty_leader0 + (uint32_t)(acc * 8));
+      if (ep.epi == kEpiArgmax && row_ok && best_i >= 0)
+        atomicMax(ep.keys + m, argmax_key(best_v, (uint32_t)best_i));
+      acc ^= 1;
+      if (acc == 0) aph ^= 1;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();   // the peer's MMAs / arrives are done before TMEM goes away
+  if (warp == 1) tmem_dealloc_pair(tmem, Cfg::kTmemCols);
+}
+
+template <int BN, int STAGES>
+cudaError_t launch_tc2(const CUtensorMap& ta, const CUtensorMap& tw, const GemmArgs& g,
+                       const EpiParams& ep, cudaStream_t s) {
+  using Cfg = Tc2Cfg<BN, STAGES>;
+  static_assert(Cfg::kSmem <= 227 * 1024, "pair GEMM stage ring exceeds shared memory");
+  auto kern = gemm_tc2_kernel<BN, STAGES>;
+  cudaError_t e = set_max_smem((const void*)kern);
+  if (e != cudaSuccess) return e;
+  const int tiles_n = (g.N + BN - 1) / BN;
+  const int tiles = tiles_n * ((g.M + 2 * kBM - 1) / (2 * kBM));
+  const int pairs = std::min(tiles, num_sms() / 2);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(2 * pairs);
+  cfg.blockDim = dim3(kTcThreads);
+  cfg.dynamicSmemBytes = Cfg::kSmem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  const uint32_t idesc = umma_idesc_f16(2 * kBM, BN, g.in_dtype == kBF16);
+  return cudaLaunchKernelEx(&cfg, kern, ta, tw, g.K, idesc, ep, tiles_n, tiles);
+}
+
 // kEpiNorm: clusters of CN CTAs along N (one per N tile of a row block).
 template <int BN, int STAGES, int CN>
 cudaError_t launch_tc_norm(const CUtensorMap& ta, const CUtensorMap& tw, const GemmArgs& g,
@@ -819,6 +1007,16 @@ bool gemm_norm_supported(int N, int in_dtype) {
 }
 
 int gemm_tile_n() { return kWBox; }
+
+// CTA-pair (cta_group::2) tiles for the large GEMMs: opt-in (FNMT_GEMM_PAIR=1)
+bool pair_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("FNMT_GEMM_PAIR");
+    on = e && e[0] == '1';
+  }
+  return on != 0;
+}
 
 bool dual_cta_enabled() {
   static int on = -1;
@@ -957,6 +1155,9 @@ cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t s) {
     return g.topk.K == 4 ? launch_tc<256, 4, 4>(*pa, *pw, g, ep, s)
                          : launch_tc<256, 4, 8>(*pa, *pw, g, ep, s);
   }
+  if (pair_enabled() && (g.epi == kEpiStore || g.epi == kEpiArgmax) &&
+      (int64_t)((g.M + 2 * kBM - 1) / (2 * kBM)) * ((g.N + 255) / 256) >= num_sms() / 2)
+    return launch_tc2<256, 6>(*pa, *pw, g, ep, s);
   switch (pick_bn(g.M, g.N)) {
     case 256: return launch_tc<256, 4>(*pa, *pw, g, ep, s);
     case 128: return launch_tc<128, 6>(*pa, *pw, g, ep, s);

@@ -248,3 +248,18 @@ def test_linear_add_norm_fused(dt, M, N, K, l1):
     got = X.cpu().numpy()
     assert np.abs(got - want).max() <= 2e-3 * max(1.0, np.abs(want).max())
     assert np.allclose(Xa.float().cpu().numpy(), got, atol=3e-2, rtol=1e-2)
+
+
+def test_cta_pair_gemm():
+    """cta_group::2 (M = 256 per CTA pair) GEMM, opt-in via FNMT_GEMM_PAIR=1;
+    run in a subprocess so the switch is read fresh and a hang cannot stall
+    the suite."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    env = dict(os.environ, FNMT_GEMM_PAIR="1")
+    r = subprocess.run([sys.executable, str(Path(__file__).parent / "pair_gemm_check.py")],
+                       env=env, capture_output=True, text=True, timeout=180)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "pair gemm ok" in r.stdout

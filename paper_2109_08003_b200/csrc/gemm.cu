@@ -1008,7 +1008,11 @@ bool gemm_norm_supported(int N, int in_dtype) {
 
 int gemm_tile_n() { return kWBox; }
 
-// CTA-pair (cta_group::2) tiles for the large GEMMs: opt-in (FNMT_GEMM_PAIR=1)
+// CTA-pair (cta_group::2) tiles for the large GEMMs: opt-in (FNMT_GEMM_PAIR=1).  Correct
+// (tests/pair_gemm_check.py) but r01 measured no gain: 6-1-1 bench 6.72M vs 6.82M words/s
+// (vocab 29.3 vs 25.1 ms per 16k sentences, encoder GEMMs equal), Deep beam 4 0.426M vs
+// 0.422M — the single-CTA 128 x 256 tiles are not L2-bandwidth bound at these shapes (the
+// vocab GEMM alone reaches 1479 TFLOP/s at 9216 rows, profiles/r01c_step_analysis.md).
 bool pair_enabled() {
   static int on = -1;
   if (on < 0) {

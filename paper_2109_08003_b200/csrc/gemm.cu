@@ -761,10 +761,7 @@ cudaError_t launch_tc(const CUtensorMap& ta, const CUtensorMap& tw, const GemmAr
   if (e != cudaSuccess) return e;
   const int tiles_n = (g.N + BN - 1) / BN;
   const int tiles = tiles_n * ((g.M + kBM - 1) / kBM);
-  int grid = tiles < MINB * num_sms() ? tiles : MINB * num_sms();
-  // decode-size GEMMs (M <= 4096): optionally fewer, longer-lived CTAs so that
-  // concurrent decode lanes' kernels keep the remaining SMs (FNMT_GEMM_GRID_CAP)
-  if (g.M <= 4096 && decode_grid_cap() > 0 && grid > decode_grid_cap()) grid = decode_grid_cap();
+  const int grid = tiles < MINB * num_sms() ? tiles : MINB * num_sms();
   const uint32_t idesc = I8 ? umma_idesc_i8(kBM, BN) : umma_idesc_f16(kBM, BN, g.in_dtype == kBF16);
   return launch_k(kern, dim3(grid), dim3(kTcThreads),
                   (size_t)Cfg::kSmem, s, ta, tw, I8 ? g.Kp : g.K, idesc, ep, tiles_n, tiles);
@@ -1023,16 +1020,6 @@ bool pair_enabled() {
     on = e && e[0] == '1';
   }
   return on != 0;
-}
-
-int decode_grid_cap() {
-  static int cap = -1;
-  if (cap < 0) {
-    const char* e = getenv("FNMT_GEMM_GRID_CAP");
-    cap = e ? atoi(e) : 0;
-    if (cap < 0) cap = 0;
-  }
-  return cap;
 }
 
 bool dual_cta_enabled() {

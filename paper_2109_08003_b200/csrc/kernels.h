@@ -31,7 +31,6 @@ inline cudaError_t set_max_smem(const void* func) {
 // their predecessor's data (common.cuh).
 bool pdl_enabled();
 bool dual_cta_enabled();   // FNMT_GEMM_DUAL=0 disables 2-CTA/SM decoder GEMMs
-int decode_grid_cap();     // FNMT_GEMM_GRID_CAP: max CTAs for M <= 4096 GEMMs (0 = off)
 bool pair_enabled();       // FNMT_GEMM_PAIR=1: cta_group::2 256-row tiles for large GEMMs
 template <typename... KArgs, typename... Args>
 cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,

@@ -62,6 +62,7 @@ class RunConfig:
     pretokenized: bool = False
     max_len_ratio: float = 1.5
     max_len_offset: int = 5
+    devices: tuple = (0,)           # GPUs (one engine each; chunk groups round-robin)
 
     def __post_init__(self):
         if self.precision not in PRECISIONS:
@@ -69,6 +70,9 @@ class RunConfig:
         for name in ("sbatch", "wbatch", "workers", "chunk_lines", "beam"):
             if getattr(self, name) < 1:
                 raise ValueError(f"{name} must be >= 1")
+        if not self.devices or any(int(d) < 0 for d in self.devices):
+            raise ValueError("devices must list at least one CUDA ordinal")
+        object.__setattr__(self, "devices", tuple(int(d) for d in self.devices))
 
 
 @dataclass
@@ -90,7 +94,10 @@ class Translator:
         self.codec = codec
         self.run = run
         self.weights = weights
-        self.engine = Engine(self.cfg, weights, dtype=run.precision, device=device)
+        devs = run.devices if run.devices != (0,) else (device,)
+        # one engine (weights + workspace + CUDA graphs) per listed device
+        self.engines = [Engine(self.cfg, weights, dtype=run.precision, device=d) for d in devs]
+        self.engine = self.engines[0]
         self.limit = max(1, min(HARD_SPLIT, self.cfg.max_positions))
 
     @classmethod
@@ -105,8 +112,9 @@ class Translator:
         t = object.__new__(Translator)
         t.__dict__.update(self.__dict__)
         new = replace(self.run, **changes)
-        if new.precision != self.run.precision:
-            raise ValueError("precision is fixed at construction (weights are uploaded once)")
+        if new.precision != self.run.precision or new.devices != self.run.devices:
+            raise ValueError("precision and devices are fixed at construction "
+                             "(weights are uploaded once)")
         t.run = new
         return t
 
@@ -136,7 +144,8 @@ class Translator:
         return res
 
     # ---- GPU stage -----------------------------------------------------------
-    def _translate_pieces(self, pieces: list) -> list:
+    def _translate_pieces(self, pieces: list, engine=None) -> list:
+        engine = engine or self.engine
         n = len(pieces)
         if n == 0:
             return []
@@ -145,7 +154,7 @@ class Translator:
         np.cumsum(lengths, out=offsets[1:])
         ids = np.concatenate(pieces).astype(np.int32) if offsets[-1] else np.zeros(1, np.int32)
         r = self.run
-        out_ids, out_len, out_off, _ = self.engine.translate(
+        out_ids, out_len, out_off, _ = engine.translate(
             ids, offsets, sbatch=r.sbatch, wbatch=r.wbatch, ratio=r.max_len_ratio,
             offset=r.max_len_offset, beam=r.beam)
         return [out_ids[o:o + L] for o, L in zip(out_off.tolist(), out_len.tolist())]
@@ -162,34 +171,44 @@ class Translator:
         return [bounds[i:i + per] for i in range(0, len(bounds), per)]
 
     def translate_lines(self, lines: Sequence[str]) -> list:
+        """Groups of chunks go round-robin to the engines (one per device), each
+        engine thread translating its groups in order while the text pool
+        tokenizes the engine's next group and detokenizes finished ones."""
         lines = list(lines)
         if not lines:
             return []
         groups = self._groups(len(lines))
-        out: list = []
+        n_eng = len(self.engines)
+        posted: list = [None] * len(groups)     # per group: futures of detokenized chunks
         with ThreadPoolExecutor(max_workers=self.run.workers) as pool:
-            def prep(group):
-                return [pool.submit(self._to_ids, lines[s:e]) for s, e in group]
+            def prep(gi):
+                return [pool.submit(self._to_ids, lines[s:e]) for s, e in groups[gi]]
 
-            pending_pre = prep(groups[0])
-            pending_post = []
-            for gi, group in enumerate(groups):
-                chunks = []
-                for ci, f in enumerate(pending_pre):
+            def lane(e):
+                mine = list(range(e, len(groups), n_eng))
+                pending = prep(mine[0]) if mine else []
+                for k, gi in enumerate(mine):
                     try:
-                        chunks.append(f.result())
+                        chunks = [f.result() for f in pending]
                     except Exception as exc:   # noqa: BLE001
                         raise ChunkFailure(gi, exc) from exc
-                if gi + 1 < len(groups):
-                    pending_pre = prep(groups[gi + 1])      # overlaps the engine call
-                flat = [p for c in chunks for p in c.pieces]
-                res = self._translate_pieces(flat)
-                k = 0
-                for c in chunks:
-                    pending_post.append(pool.submit(self._to_text, c, res[k:k + len(c.pieces)]))
-                    k += len(c.pieces)
-            for f in pending_post:
-                out.extend(f.result())
+                    if k + 1 < len(mine):
+                        pending = prep(mine[k + 1])     # overlaps this group's engine call
+                    res = self._translate_pieces([p for c in chunks for p in c.pieces],
+                                                 self.engines[e])
+                    futs, o = [], 0
+                    for c in chunks:
+                        futs.append(pool.submit(self._to_text, c, res[o:o + len(c.pieces)]))
+                        o += len(c.pieces)
+                    posted[gi] = futs
+
+            if n_eng == 1:
+                lane(0)
+            else:
+                with ThreadPoolExecutor(max_workers=n_eng) as gpus:
+                    for f in [gpus.submit(lane, e) for e in range(n_eng)]:
+                        f.result()
+            out = [y for futs in posted for f in futs for y in f.result()]
         if len(out) != len(lines):
             raise ChunkFailure(0, ValueError(f"{len(out)} lines out for {len(lines)} in"))
         return out
@@ -213,7 +232,8 @@ class Translator:
             "target_words": tgt_words,
             "target_words_per_second": tgt_words / wall,
             "sentences_per_second": len(lines) / wall,
-            "est_peak_bytes": int(self.engine.device_bytes()),
+            "est_peak_bytes": int(max(e.device_bytes() for e in self.engines)),
+            "devices": len(self.engines),
             "sbatch": self.run.sbatch,
             "wbatch": self.run.wbatch,
             "workers": self.run.workers,

@@ -136,3 +136,21 @@ def test_cli_translate_bench_selftest(tmp_path):
     r = run_cli("selftest")
     assert r.returncode == 0, r.stdout + r.stderr
     assert b"selftest=pass" in r.stdout
+
+
+def test_multi_engine_translate_identical(tr16):
+    """devices=(0, 0): two engines (the multi-GPU layout, here on one GPU) with
+    chunk groups round-robin — output identical to one engine."""
+    cfg, w, vocab, codec = assets()
+    lines = TR["lines"] * 3
+    one = tr16.with_run(chunk_lines=5).translate_lines(lines)
+    import paper_2109_08003_b200.translator as trm
+    old = trm.GPU_GROUP_LINES
+    trm.GPU_GROUP_LINES = 10          # several groups per engine
+    try:
+        two = Translator(cfg, w, vocab, codec=codec,
+                         run=RunConfig(precision="f16", chunk_lines=5, devices=(0, 0)))
+        assert two.translate_lines(lines) == one
+        assert two.bench(lines[:10])["devices"] == 2
+    finally:
+        trm.GPU_GROUP_LINES = old

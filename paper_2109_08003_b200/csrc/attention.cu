@@ -356,7 +356,11 @@ __global__ void __launch_bounds__(NT) attn_decode_kernel(DecAttnArgs a, float qs
       }
 #pragma unroll
       for (int o = G / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (li == 0 && j < c.nk) S[j] = c.all_masked ? s + kMaskValue : s;
+      if (li == 0 && j < c.nk) {
+        if (a.kc_off >= 0)   // folded cross attention: + qscale * (b_q . k_j)
+          s += qscale * to_f32(kb[decode_key_row(a, c, r, j) * a.ldkv + a.kc_off - h * dk]);
+        S[j] = c.all_masked ? s + kMaskValue : s;
+      }
     }
   }
   __syncthreads();
@@ -395,6 +399,15 @@ __global__ void __launch_bounds__(NT) attn_decode_kernel(DecAttnArgs a, float qs
     for (int i = 0; i < VEC; ++i) red[grp * dk + ch * VEC + i] = acc[i];
   }
   __syncthreads();
+  if (a.out_f32) {   // folded cross attention: o-projection output in fp32 (+ its bias)
+    float* out = reinterpret_cast<float*>(a.out) + (size_t)r * a.ldo + h * dk;
+    for (int e = tid; e < dk; e += NT) {
+      float sum = red[e];
+      for (int gg = 1; gg < groups; ++gg) sum += red[gg * dk + e];
+      out[e] = a.out_bias ? sum + a.out_bias[h * dk + e] : sum;
+    }
+    return;
+  }
   T* out = reinterpret_cast<T*>(a.out) + (size_t)r * a.ldo + h * dk;
   for (int e = tid; e < dk; e += NT) {
     float sum = red[e];
@@ -790,6 +803,11 @@ cudaError_t launch_dec_async(const DecAttnArgs& a, float qscale, cudaStream_t s)
 
 template <typename T, int G, int CH>
 cudaError_t launch_dec(const DecAttnArgs& a, float qscale, cudaStream_t s) {
+  if (a.kc_off >= 0 || a.out_f32) {   // folded cross attention: two-pass kernel only
+    if (G != 32 || a.heads != 1) return cudaErrorInvalidValue;
+    if ((int64_t)a.rows < 1200) return launch_dec_nt<T, G, CH, 512>(a, qscale, s);
+    return launch_dec_nt<T, G, CH, 128>(a, qscale, s);
+  }
   // few (row, head) blocks -> wide blocks so the SMs still have enough warps in flight
   // cp.async staging measured faster for 8 heads (dk=64) only (r01: 6-1-8 3.92M vs 3.67M
   // words/s; 6-1-1 3.92M vs 4.32M)

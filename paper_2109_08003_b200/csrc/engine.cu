@@ -404,6 +404,78 @@ Norm Engine::make_norm(const std::string& prefix) {
   return Norm{upload_f32(need(prefix + ".gain", d)), upload_f32(need(prefix + ".bias", d))};
 }
 
+// Folded cross attention weights of decoder layer `prefix` (reference
+// orientation x @ W, all [d, d]): rows of W^T [2d + 8, d]
+//   a < d      : (Wk Wq^T)^T  -> K~ = E (Wk Wq^T) + bk Wq^T          (K Wq^T)
+//   d + c      : (Wv Wo)^T    -> V~ = E (Wv Wo) + bv Wo              (V Wo)
+//   2d         : Wk bq        -> c  = E (Wk bq) + bk . bq            (bq . k)
+//   2d+1..2d+7 : 0 (16-byte row alignment)
+// so q.k = x.K~ + c and (sum_j p_j v_j) Wo + bo = sum_j p_j V~_j + bo: the
+// per-step cross-q and cross-o GEMMs disappear (model.py:331-336 reassociated;
+// computed in double, rounded once to the compute dtype).
+Lin Engine::make_folded_cross(const std::string& p) {
+  const int d = arch.d_model, N = 2 * d + 8;
+  const auto& Wq = need(p + ".cross.q_w", (int64_t)d * d);
+  const auto& Wk = need(p + ".cross.k_w", (int64_t)d * d);
+  const auto& Wv = need(p + ".cross.v_w", (int64_t)d * d);
+  const auto& Wo = need(p + ".cross.o_w", (int64_t)d * d);
+  const auto& bq = need(p + ".cross.q_b", d);
+  const auto& bk = need(p + ".cross.k_b", d);
+  const auto& bv = need(p + ".cross.v_b", d);
+  std::vector<double> woT((size_t)d * d);   // woT[c][n] = Wo[n][c]
+  for (int n = 0; n < d; ++n)
+    for (int c = 0; c < d; ++c) woT[(size_t)c * d + n] = Wo[(size_t)n * d + c];
+  std::vector<float> wt((size_t)N * d, 0.f), bias(N, 0.f);
+  for (int a = 0; a < d; ++a) {
+    const float* q = &Wq[(size_t)a * d];
+    for (int b = 0; b < d; ++b) {
+      const float* k = &Wk[(size_t)b * d];
+      double acc = 0.0;
+      for (int n = 0; n < d; ++n) acc += (double)k[n] * q[n];
+      wt[(size_t)a * d + b] = (float)acc;
+    }
+    double bb = 0.0;
+    for (int n = 0; n < d; ++n) bb += (double)bk[n] * q[n];
+    bias[a] = (float)bb;
+  }
+  for (int c = 0; c < d; ++c) {
+    const double* o = &woT[(size_t)c * d];
+    for (int b = 0; b < d; ++b) {
+      const float* v = &Wv[(size_t)b * d];
+      double acc = 0.0;
+      for (int n = 0; n < d; ++n) acc += (double)v[n] * o[n];
+      wt[(size_t)(d + c) * d + b] = (float)acc;
+    }
+    double bb = 0.0;
+    for (int n = 0; n < d; ++n) bb += (double)bv[n] * o[n];
+    bias[d + c] = (float)bb;
+  }
+  for (int b = 0; b < d; ++b) {
+    double acc = 0.0;
+    for (int n = 0; n < d; ++n) acc += (double)Wk[(size_t)b * d + n] * bq[n];
+    wt[(size_t)(2 * d) * d + b] = (float)acc;
+  }
+  double bc = 0.0;
+  for (int n = 0; n < d; ++n) bc += (double)bk[n] * bq[n];
+  bias[2 * d] = (float)bc;
+  Lin L;
+  L.N = N;
+  L.K = d;
+  L.w = upload_act(wt);
+  L.b = upload_f32(bias);
+  finish_lin(L);
+  return L;
+}
+
+bool fused_cross_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("FNMT_FUSED_CROSS");
+    on = !(e && e[0] == '0');
+  }
+  return on != 0;
+}
+
 void Engine::finalize() {
   CK(cudaSetDevice(device));
   const int d = arch.d_model, V = arch.vocab_size;
@@ -454,6 +526,9 @@ void Engine::finalize() {
     L.n2 = make_norm(p + ".norm2");
     enc.push_back(L);
   }
+  fused_cross = dt != kF32 && !q8 && arch.n_heads_dec == 1 && d % 256 == 0 &&
+                fused_cross_enabled();
+  ckv_ld = fused_cross ? 2 * d + 8 : 2 * d;
   dec.clear();
   for (int i = 0; i < arch.n_dec_layers; ++i) {
     const std::string p = "dec." + std::to_string(i);
@@ -465,6 +540,7 @@ void Engine::finalize() {
     L.ckv = make_lin({p + ".cross.k_w", p + ".cross.v_w"}, {p + ".cross.k_b", p + ".cross.v_b"},
                      d, {d, d});
     L.co = make_lin({p + ".cross.o_w"}, {p + ".cross.o_b"}, d, {d});
+    if (fused_cross) L.fck = make_folded_cross(p);
     L.n1 = make_norm(p + ".norm1");
     L.n2 = make_norm(p + ".norm2");
     L.ffn = arch.ffn_dim_dec > 0;
@@ -525,7 +601,7 @@ void Engine::reserve(int tok_cap, int row_cap, int64_t pool_cap) {
   ws.kc.assign(arch.n_dec_layers, nullptr);
   ws.vc.assign(arch.n_dec_layers, nullptr);
   for (int l = 0; l < arch.n_dec_layers; ++l) {
-    ws.ckv[l] = alloc((size_t)es * tok_cap * 2 * d);
+    ws.ckv[l] = alloc((size_t)es * tok_cap * ckv_ld);
     ws.kc[l] = alloc((size_t)es * pool_cap * d);
     ws.vc[l] = alloc((size_t)es * pool_cap * d);
   }
@@ -564,7 +640,8 @@ void Engine::reserve(int tok_cap, int row_cap, int64_t pool_cap) {
     // (q load, 4 barriers, 1-warp softmax) dominates once the producer runs ahead.
     const int dkd = d / arch.n_heads_dec;
     const char* env = getenv("FNMT_DECODE_TMA");
-    ws.kv_tma = env && env[0] == '1' && dkd % 8 == 0 && (dkd <= 256 || dkd % 256 == 0);
+    ws.kv_tma = env && env[0] == '1' && !fused_cross && dkd % 8 == 0 &&
+                (dkd <= 256 || dkd % 256 == 0);
     ws.tm_sk.resize(arch.n_dec_layers);
     ws.tm_sv.resize(arch.n_dec_layers);
     ws.tm_ckv.resize(arch.n_dec_layers);
@@ -739,7 +816,8 @@ void Engine::cross_kv_all(int n_tok, cudaStream_t s) {
   const int d = arch.d_model;
   gemm_cls = FNMT_K_GEMM_ENC;
   for (int l = 0; l < arch.n_dec_layers; ++l)
-    gemm(ws.xa, dt != kF32 ? &ws.tm_xa : nullptr, d, dec[l].ckv, n_tok, ws.ckv[l], 2 * d, dt, 0, s);
+    gemm(ws.xa, dt != kF32 ? &ws.tm_xa : nullptr, d, fused_cross ? dec[l].fck : dec[l].ckv, n_tok,
+         ws.ckv[l], ckv_ld, dt, 0, s);
 }
 
 // One decoder step for v.rows rows (model.py:308-344).  All sizes that vary
@@ -822,15 +900,23 @@ void Engine::run_step(const StepView& v, cudaStream_t s) {
     }
     ++launches;
     gemm_norm(ws.datt, tc ? &ws.tm_datt : nullptr, d, L.so, R, ws.dx32, ws.dxa, ws.dy32, L.n1, s);
-    gemm(ws.dxa, tc ? &ws.tm_dxa : nullptr, d, L.cq, R, ws.dq, d, dt, 0, s);
+    // folded cross attention (workspace caches only): q is the norm1 output itself,
+    // the attention writes the o-projection output (fp32, + bias) straight into dy32
+    const bool folded = fused_cross && v.ws_caches;
+    if (!folded) gemm(ws.dxa, tc ? &ws.tm_dxa : nullptr, d, L.cq, R, ws.dq, d, dt, 0, s);
     DecAttnArgs c{};
-    c.q = ws.dq;
+    c.q = folded ? ws.dxa : ws.dq;
     c.ldq = d;
     c.k = v.ckv[l];
     c.v = (const char*)v.ckv[l] + (size_t)d * es;
-    c.ldkv = 2 * d;
-    c.out = ws.datt;
+    c.ldkv = v.ws_caches ? ckv_ld : 2 * d;
+    c.out = folded ? (void*)ws.dy32 : ws.datt;
     c.ldo = d;
+    if (folded) {
+      c.kc_off = 2 * d;
+      c.out_f32 = 1;
+      c.out_bias = L.co.b;
+    }
     c.dtype = dt;
     c.heads = arch.n_heads_dec;
     c.dk = d / arch.n_heads_dec;
@@ -850,7 +936,10 @@ void Engine::run_step(const StepView& v, cudaStream_t s) {
       prof_end(s, ev, FNMT_K_ATTN_DEC, 0.0, (double)R * v.max_k * 2 * d * es);
     }
     ++launches;
-    gemm_norm(ws.datt, tc ? &ws.tm_datt : nullptr, d, L.co, R, ws.dx32, ws.dxa, ws.dy32, L.n2, s);
+    if (folded)
+      norm(ws.dx32, ws.dy32, L.n2, ws.dx32, ws.dxa, R, s);
+    else
+      gemm_norm(ws.datt, tc ? &ws.tm_datt : nullptr, d, L.co, R, ws.dx32, ws.dxa, ws.dy32, L.n2, s);
     if (L.ffn) {
       gemm(ws.dxa, tc ? &ws.tm_dxa : nullptr, d, L.f1, R, ws.dh, arch.ffn_dim_dec, dt, 1, s);
       gemm_norm(ws.dh, tc ? &ws.tm_dh : nullptr, arch.ffn_dim_dec, L.f2, R, ws.dx32, ws.dxa, ws.dy32,
@@ -1060,6 +1149,8 @@ std::unique_ptr<Engine> Engine::make_lane() {
   L->enc = enc;
   L->dec = dec;
   L->finalized = true;   // weights are shared (owned by this engine)
+  L->fused_cross = fused_cross;
+  L->ckv_ld = ckv_ld;
   L->n_lanes = 1;
   return L;
 }

@@ -54,6 +54,7 @@ struct EncL {
 };
 struct DecL {
   Lin sqkv, so, cq, ckv, co, f1, f2;
+  Lin fck;   // folded cross K|V|c (fused_cross): [K Wq^T | V Wo | bq.k] per encoder row
   Norm n1, n2, n3;
   bool ffn = false;
 };
@@ -156,6 +157,11 @@ class Engine {
   void set_qtensor(const std::string& name, const int8_t* q, const float* scale, const float* zp,
                    int64_t k, int64_t n);
   bool q8 = false;   // int8 GEMM weights (dtype code 3): activations stay f32
+  // Folded cross attention for single-head decoders (fp16 / bf16): the cross
+  // query and output projections are multiplied into the per-batch cross K/V
+  // (K~ = K Wq^T, V~ = V Wo, c = bq.k), removing two GEMMs from every step.
+  bool fused_cross = false;
+  int ckv_ld = 0;    // row stride (elements) of the workspace cross K/V
   void finalize();
   void reserve(int tok_cap, int row_cap, int64_t pool_cap);
   void reserve_for(const fnmt_run& run);
@@ -220,6 +226,7 @@ class Engine {
   void* upload_act(const std::vector<float>& v);
   Lin make_lin(const std::vector<std::string>& wnames, const std::vector<std::string>& bnames,
                int k, const std::vector<int>& ns);
+  Lin make_folded_cross(const std::string& prefix);
   void finish_lin(Lin& L);
   void make_qlin(Lin& L, const std::vector<std::string>& wnames, int k, const std::vector<int>& ns);
   void attach_q(GemmArgs& g, const Lin& L) const;

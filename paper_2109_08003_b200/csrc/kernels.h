@@ -207,6 +207,13 @@ struct DecAttnArgs {
   int64_t anc_buf_stride;               // elements between the two tables (step parity t & 1)
   const int32_t* k_start; const int32_t* k_len; int k_pad; int rows_per_seq;
   int max_k;
+  // folded cross attention (engine.cu, fused_cross): each key row also carries
+  // a per-key score offset at column kc_off (added as qscale * c_j; -1 = none),
+  // and the output is written in fp32 with out_bias added (the o-projection's
+  // bias: the values are already o-projected).
+  int kc_off = -1;
+  const float* out_bias = nullptr;
+  int out_f32 = 0;
 };
 cudaError_t launch_attention_decode(const DecAttnArgs& a, cudaStream_t s);
 

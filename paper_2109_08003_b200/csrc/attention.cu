@@ -801,12 +801,36 @@ cudaError_t launch_dec_async(const DecAttnArgs& a, float qscale, cudaStream_t s)
                   a, qscale);
 }
 
+// block width for the two-pass kernel: few (row, head) blocks -> wider blocks.
+// FNMT_DEC_NT: 0 = auto (< FNMT_DEC_FEW rows x heads -> 512 threads, else 128),
+// or a fixed 128 / 256 / 512.
+int dec_nt_choice(int64_t blocks) {
+  static int fixed = -1, few = -1;
+  if (fixed < 0) {
+    const char* e = getenv("FNMT_DEC_NT");
+    fixed = e ? atoi(e) : 0;
+    if (fixed != 128 && fixed != 256 && fixed != 512) fixed = 0;
+    const char* f = getenv("FNMT_DEC_FEW");
+    few = f ? atoi(f) : 1200;
+  }
+  if (fixed) return fixed;
+  return blocks < few ? 512 : 128;
+}
+
+template <typename T, int G, int CH>
+cudaError_t launch_dec_wide(const DecAttnArgs& a, float qscale, cudaStream_t s) {
+  switch (dec_nt_choice((int64_t)a.rows * a.heads)) {
+    case 512: return launch_dec_nt<T, G, CH, 512>(a, qscale, s);
+    case 256: return launch_dec_nt<T, G, CH, 256>(a, qscale, s);
+    default: return launch_dec_nt<T, G, CH, 128>(a, qscale, s);
+  }
+}
+
 template <typename T, int G, int CH>
 cudaError_t launch_dec(const DecAttnArgs& a, float qscale, cudaStream_t s) {
   if (a.kc_off >= 0 || a.out_f32) {   // folded cross attention: two-pass kernel only
     if (G != 32 || a.heads != 1) return cudaErrorInvalidValue;
-    if ((int64_t)a.rows < 1200) return launch_dec_nt<T, G, CH, 512>(a, qscale, s);
-    return launch_dec_nt<T, G, CH, 128>(a, qscale, s);
+    return launch_dec_wide<T, G, CH>(a, qscale, s);
   }
   // few (row, head) blocks -> wide blocks so the SMs still have enough warps in flight
   // cp.async staging measured faster for 8 heads (dk=64) only (r01: 6-1-8 3.92M vs 3.67M
@@ -815,8 +839,7 @@ cudaError_t launch_dec(const DecAttnArgs& a, float qscale, cudaStream_t s) {
     if ((int64_t)a.rows * a.heads < 1200) return launch_dec_async<T, G, CH, 256>(a, qscale, s);
     return launch_dec_async<T, G, CH, 128>(a, qscale, s);
   }
-  if ((int64_t)a.rows * a.heads < 1200) return launch_dec_nt<T, G, CH, 512>(a, qscale, s);
-  return launch_dec_nt<T, G, CH, 128>(a, qscale, s);
+  return launch_dec_wide<T, G, CH>(a, qscale, s);
 }
 
 bool dec_rows_enabled() {

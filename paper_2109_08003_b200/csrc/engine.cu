@@ -467,6 +467,15 @@ Lin Engine::make_folded_cross(const std::string& p) {
   return L;
 }
 
+bool fold_norm_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("FNMT_FOLD_NORM");
+    on = !(e && e[0] == '0');
+  }
+  return on != 0;
+}
+
 bool fused_cross_enabled() {
   static int on = -1;
   if (on < 0) {
@@ -916,6 +925,13 @@ void Engine::run_step(const StepView& v, cudaStream_t s) {
       c.kc_off = 2 * d;
       c.out_f32 = 1;
       c.out_bias = L.co.b;
+      if (fold_norm_enabled()) {   // + residual + norm2 in the same kernel
+        c.nx = ws.dx32;
+        c.nx_act = ws.dxa;
+        c.ngain = L.n2.g;
+        c.nbeta = L.n2.b;
+        c.nl1 = arch.norm_l1;
+      }
     }
     c.dtype = dt;
     c.heads = arch.n_heads_dec;
@@ -936,9 +952,9 @@ void Engine::run_step(const StepView& v, cudaStream_t s) {
       prof_end(s, ev, FNMT_K_ATTN_DEC, 0.0, (double)R * v.max_k * 2 * d * es);
     }
     ++launches;
-    if (folded)
-      norm(ws.dx32, ws.dy32, L.n2, ws.dx32, ws.dxa, R, s);
-    else
+    if (folded) {
+      if (!c.ngain) norm(ws.dx32, ws.dy32, L.n2, ws.dx32, ws.dxa, R, s);
+    } else
       gemm_norm(ws.datt, tc ? &ws.tm_datt : nullptr, d, L.co, R, ws.dx32, ws.dxa, ws.dy32, L.n2, s);
     if (L.ffn) {
       gemm(ws.dxa, tc ? &ws.tm_dxa : nullptr, d, L.f1, R, ws.dh, arch.ffn_dim_dec, dt, 1, s);

@@ -214,6 +214,13 @@ struct DecAttnArgs {
   int kc_off = -1;
   const float* out_bias = nullptr;
   int out_f32 = 0;
+  // ... and optionally the post-norm block fused in (single head, row = dk):
+  // x[r] = norm(x[r] + out) * gain + beta in place (fp32), copy in T to x_act
+  float* nx = nullptr;
+  void* nx_act = nullptr;
+  const float* ngain = nullptr;
+  const float* nbeta = nullptr;
+  int nl1 = 0;
 };
 cudaError_t launch_attention_decode(const DecAttnArgs& a, cudaStream_t s);
 

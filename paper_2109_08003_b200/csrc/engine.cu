@@ -467,11 +467,15 @@ Lin Engine::make_folded_cross(const std::string& p) {
   return L;
 }
 
+// Opt-in (FNMT_FOLD_NORM=1): residual + norm2 inside the folded cross attention kernel.
+// Correct (143 GPU tests, config-1 fp16 64/64) but r01 measured it neutral-to-slower
+// (6.94M vs 7.03M words/s): the launch it saves is hidden by the concurrent decode lanes
+// while the two block reductions lengthen the attention CTA.
 bool fold_norm_enabled() {
   static int on = -1;
   if (on < 0) {
     const char* e = getenv("FNMT_FOLD_NORM");
-    on = !(e && e[0] == '0');
+    on = e && e[0] == '1';
   }
   return on != 0;
 }

@@ -251,3 +251,17 @@ def test_folded_cross_attention_corpus_path(dtype):
         got = split_off(out, olen, off)
         same = sum(x == y for x, y in zip(got, want))
         assert same >= len(rows) - (2 if dtype == "f16" else 4), (k, same)
+
+
+def test_fold_norm_path():
+    """Opt-in FNMT_FOLD_NORM=1 (residual + norm2 inside the folded cross
+    attention) on BASELINE config 1, in a subprocess (the switch is read once)."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    env = dict(os.environ, FNMT_FOLD_NORM="1")
+    r = subprocess.run([sys.executable, str(Path(__file__).parent / "fold_norm_check.py")],
+                       env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "fold norm ok" in r.stdout

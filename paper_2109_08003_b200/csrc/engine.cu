@@ -84,6 +84,17 @@ __global__ void init_decode_kernel(int32_t* prev, uint8_t* finished, int32_t* ou
   }
 }
 
+// Reference _check_tokens (model.py:254-258): every source id in [0, V).
+__global__ void check_ids_kernel(const int32_t* __restrict__ ids, const int64_t* __restrict__ off0,
+                                 int64_t total, int V, int32_t* bad) {
+  const int64_t base = *off0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t v = ids[base + i];
+    if (v < 0 || v >= V) *bad = 1;
+  }
+}
+
 __global__ void fill_i32_kernel(int32_t* p, int n, int v) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) p[i] = v;
@@ -1021,6 +1032,20 @@ void Engine::translate_device(const int32_t* d_ids, const int64_t* d_off,
       throw EngineError(FNMT_E_LENGTH, "source length " + std::to_string(L) +
                                            " exceeds max_positions " +
                                            std::to_string(arch.max_positions));
+  }
+  {
+    int64_t total = 0;
+    for (int32_t L : lengths) total += L;
+    if (total > 0) {
+      if (!d_bad) d_bad = (int32_t*)dalloc(sizeof(int32_t));
+      CK(cudaMemsetAsync(d_bad, 0, sizeof(int32_t), stream));
+      const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 8);
+      check_ids_kernel<<<blocks, 256, 0, stream>>>(d_ids, d_off, total, arch.vocab_size, d_bad);
+      CK(cudaGetLastError());
+      CK(cudaMemcpyAsync(h_alive + 2, d_bad, sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
+      CK(cudaStreamSynchronize(stream));
+      if (h_alive[2]) throw EngineError(FNMT_E_INVALID, "token id out of range");
+    }
   }
   const int64_t launches0 = launches;
   CK(cudaEventRecord(ev_t0, stream));

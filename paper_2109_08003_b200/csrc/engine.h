@@ -273,6 +273,7 @@ class Engine {
   cudaEvent_t ev_poll[2] = {nullptr, nullptr};
   cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr;
   int32_t* h_alive = nullptr;
+  int32_t* d_bad = nullptr;   // source-id validation flag
   int32_t* meta_perm = nullptr;
   int32_t* meta_cu = nullptr;
   int32_t* meta_budget = nullptr;

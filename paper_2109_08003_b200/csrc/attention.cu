@@ -855,7 +855,8 @@ cudaError_t launch_dec_async(const DecAttnArgs& a, float qscale, cudaStream_t s)
 }
 
 // block width for the two-pass kernel: few (row, head) blocks -> wider blocks.
-// FNMT_DEC_NT: 0 = auto (< FNMT_DEC_FEW rows x heads -> 512 threads, else 128),
+// FNMT_DEC_NT: 0 = auto (< FNMT_DEC_FEW rows x heads -> 512 threads, else 128;
+// FEW default 600: r01 A/B 7.03 / 7.08 vs 6.97 / 6.99 M words/s for 1200),
 // or a fixed 128 / 256 / 512.
 int dec_nt_choice(int64_t blocks) {
   static int fixed = -1, few = -1;
@@ -864,7 +865,7 @@ int dec_nt_choice(int64_t blocks) {
     fixed = e ? atoi(e) : 0;
     if (fixed != 128 && fixed != 256 && fixed != 512) fixed = 0;
     const char* f = getenv("FNMT_DEC_FEW");
-    few = f ? atoi(f) : 1200;
+    few = f ? atoi(f) : 600;
   }
   if (fixed) return fixed;
   return blocks < few ? 512 : 128;

@@ -185,9 +185,11 @@ class Engine {
   int64_t device_bytes = 0;
   int64_t launches = 0;
 
-  // Concurrent decode lanes (engines sharing these weights); 3 by default
-  // (r01: 1 / 2 / 3 lanes = 5.10 / 5.82 / 6.00 M target words/s).
-  int n_lanes = 3;
+  // Concurrent decode lanes (engines sharing these weights); 4 by default
+  // (r01: 1 / 2 / 3 lanes = 5.10 / 5.82 / 6.00 M target words/s on the early kernels;
+  // final kernels 2 / 3 / 4 lanes = 6.71 / 6.98 / 7.04 M; each lane holds its own
+  // ~1.3 GB workspace at the 3072 / 64000 caps).
+  int n_lanes = 4;
   int64_t total_device_bytes() const {
     int64_t b = device_bytes;
     for (const auto& L : lanes) b += L->device_bytes;

@@ -324,7 +324,6 @@ template <typename T, int G, int CH, int NT, int U = 1, int UV = 1>
 __global__ void __launch_bounds__(NT) attn_decode_kernel(DecAttnArgs a, float qscale) {
   pdl_trigger();
   pdl_wait();
-  const bool dec_prefetch_v = a.prefetch_v;
   constexpr int VEC = Vec16<T>::N;
   extern __shared__ float sm[];
   const int dk = a.dk;
@@ -348,21 +347,11 @@ __global__ void __launch_bounds__(NT) attn_decode_kernel(DecAttnArgs a, float qs
     for (int u = 0; u < U; ++u) {
       const int j = j0 + u * stride + g;
       if (j < c.nk) {
-        const int64_t krow = decode_key_row(a, c, r, j);
-        const T* kr = kb + krow * a.ldkv;
+        const T* kr = kb + decode_key_row(a, c, r, j) * a.ldkv;
 #pragma unroll
         for (int ch = 0; ch < CH; ++ch) {
           const int e0 = (li + ch * G) * VEC;
           if (e0 < dk) raw[u][ch] = *reinterpret_cast<const uint4*>(kr + e0);
-        }
-        if (dec_prefetch_v) {   // pull this key's value row toward L2 for the value pass
-          const T* vr = reinterpret_cast<const T*>(a.v) + h * dk + krow * a.ldkv;
-#pragma unroll
-          for (int ch = 0; ch < CH; ++ch) {
-            const int e0 = (li + ch * G) * VEC;
-            if (e0 < dk && ((li + ch * G) & 7) == 0)   // one prefetch per 128-byte line
-              asm volatile("prefetch.global.L2 [%0];" ::"l"(vr + e0));
-          }
         }
       }
     }

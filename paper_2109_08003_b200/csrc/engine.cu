@@ -482,15 +482,6 @@ Lin Engine::make_folded_cross(const std::string& p) {
 // Correct (143 GPU tests, config-1 fp16 64/64) but r01 measured it neutral-to-slower
 // (6.94M vs 7.03M words/s): the launch it saves is hidden by the concurrent decode lanes
 // while the two block reductions lengthen the attention CTA.
-bool dec_prefetch_enabled() {
-  static int on = -1;
-  if (on < 0) {
-    const char* e = getenv("FNMT_DEC_PF");
-    on = !(e && e[0] == '0');
-  }
-  return on != 0;
-}
-
 bool fold_norm_enabled() {
   static int on = -1;
   if (on < 0) {
@@ -923,7 +914,6 @@ void Engine::run_step(const StepView& v, cudaStream_t s) {
     a.anc = v.anc;
     a.anc_buf_stride = v.anc_stride;
     a.max_k = v.cap;
-    a.prefetch_v = dec_prefetch_enabled();
     {
       const int ev = prof_begin(s);
       if (v.ws_caches && ws.kv_tma && !v.anc && tc)
@@ -968,7 +958,6 @@ void Engine::run_step(const StepView& v, cudaStream_t s) {
     c.k_pad = v.k_pad;
     c.rows_per_seq = v.rows_per_seq;
     c.max_k = v.max_k;
-    c.prefetch_v = dec_prefetch_enabled();
     {
       const int ev = prof_begin(s);
       if (v.ws_caches && ws.kv_tma && tc)

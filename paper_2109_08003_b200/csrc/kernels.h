@@ -216,7 +216,6 @@ struct DecAttnArgs {
   int out_f32 = 0;
   // ... and optionally the post-norm block fused in (single head, row = dk):
   // x[r] = norm(x[r] + out) * gain + beta in place (fp32), copy in T to x_act
-  int prefetch_v = 0;   // two-pass kernel: L2-prefetch each key's value row in the score pass
   float* nx = nullptr;
   void* nx_act = nullptr;
   const float* ngain = nullptr;

@@ -804,18 +804,9 @@ cudaError_t varlen_dispatch(const AttnArgs& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-// FNMT_DEC_U = score rounds x 10 + value rows in flight (11, 14, 18, 24, 28);
-// r01 A/B (6-1-1 bench): 11 6.82M, 14 6.86M, 18 6.47M, 24 6.87M, 28 6.70M words/s
-int dec_unroll() {
-  static int u = -1;
-  if (u < 0) {
-    const char* e = getenv("FNMT_DEC_U");
-    u = e ? atoi(e) : 24;
-    if (u != 11 && u != 14 && u != 18 && u != 28) u = 24;
-  }
-  return u;
-}
-
+// Two-pass kernel unroll: 2 score rounds / 4 value rows in flight per warp /
+// thread (r01 A/B of (U, UV) = (1,1) (1,4) (1,8) (2,4) (2,8): 6.82 / 6.86 / 6.47 /
+// 6.87 / 6.70 M words/s).
 template <typename T, int G, int CH, int NT, int U, int UV>
 cudaError_t launch_dec_nt_u(const DecAttnArgs& a, float qscale, cudaStream_t s) {
   const int groups = NT / (a.dk / Vec16<T>::N);
@@ -831,13 +822,7 @@ cudaError_t launch_dec_nt_u(const DecAttnArgs& a, float qscale, cudaStream_t s) 
 
 template <typename T, int G, int CH, int NT>
 cudaError_t launch_dec_nt(const DecAttnArgs& a, float qscale, cudaStream_t s) {
-  switch (dec_unroll()) {
-    case 14: return launch_dec_nt_u<T, G, CH, NT, 1, 4>(a, qscale, s);
-    case 18: return launch_dec_nt_u<T, G, CH, NT, 1, 8>(a, qscale, s);
-    case 24: return launch_dec_nt_u<T, G, CH, NT, 2, 4>(a, qscale, s);
-    case 28: return launch_dec_nt_u<T, G, CH, NT, 2, 8>(a, qscale, s);
-    default: return launch_dec_nt_u<T, G, CH, NT, 1, 1>(a, qscale, s);
-  }
+  return launch_dec_nt_u<T, G, CH, NT, 2, 4>(a, qscale, s);
 }
 
 template <typename T, int G, int CH, int NT>

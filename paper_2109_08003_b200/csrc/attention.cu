@@ -607,192 +607,6 @@ __global__ void __launch_bounds__(NT) attn_decode_rows_kernel(DecAttnArgs a, flo
   }
 }
 
-
-// Single-head decode attention, one WARP per row (fp16 / bf16, dk = 256 CH).
-// No block barriers: the warp streams its row's keys U at a time (each lane
-// holds CH 16-byte chunks of a key), reduces each score with shuffles, keeps
-// the scores in its own smem slice, normalises them (max shift, exp, divide
-// by the sum: tensor.py:70-81) and streams the values U at a time into
-// per-lane accumulators.  Many rows per CTA / SM hide the load latency that a
-// CTA-per-row kernel spends in its three __syncthreads phases.  Same
-// folded-cross options (kc_off, out_f32 / out_bias) as attn_decode_kernel.
-template <typename T, int CH, int U, int WPC>
-__global__ void __launch_bounds__(WPC * 32) attn_decode_warp_kernel(DecAttnArgs a, float qscale) {
-  pdl_trigger();
-  pdl_wait();
-  constexpr int VEC = Vec16<T>::N;
-  extern __shared__ float sm[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int r = blockIdx.x * WPC + warp;
-  if (r >= a.rows) return;
-  float* S = sm + (size_t)warp * a.max_k;
-  const int dk = a.dk;
-  DecCtx c{};
-  if (a.self_mode) {
-    c.t = *a.t_ptr;
-    c.nk = c.t + 1;
-    if (a.new_k) {
-      T* kw = reinterpret_cast<T*>(a.k_w);
-      T* vw = reinterpret_cast<T*>(a.v_w);
-      const T* nkp = reinterpret_cast<const T*>(a.new_k) + (size_t)r * a.ld_new;
-      const T* nvp = reinterpret_cast<const T*>(a.new_v) + (size_t)r * a.ld_new;
-      const size_t slot = ((size_t)r * a.cap + c.t) * a.ldkv;
-      for (int e = lane; e < dk; e += 32) {
-        kw[slot + e] = nkp[e];
-        vw[slot + e] = nvp[e];
-      }
-      __syncwarp();
-    }
-  } else {
-    const int seq = r / a.rows_per_seq;
-    const int kl = a.k_len[seq];
-    c.all_masked = kl == 0;
-    c.nk = c.all_masked ? a.k_pad : kl;
-    c.seq_row0 = a.k_start[seq];
-  }
-  float qf[CH][VEC];
-  {
-    const T* q = reinterpret_cast<const T*>(a.q) + (size_t)r * a.ldq;
-#pragma unroll
-    for (int ch = 0; ch < CH; ++ch) {
-      cvt16<T>(*reinterpret_cast<const uint4*>(q + (lane + ch * 32) * VEC), qf[ch]);
-#pragma unroll
-      for (int i = 0; i < VEC; ++i) qf[ch][i] *= qscale;
-    }
-  }
-  const T* kb = reinterpret_cast<const T*>(a.k);
-  const T* vb = reinterpret_cast<const T*>(a.v);
-  const int nk = c.nk;
-  float mx = -INFINITY;
-  for (int j0 = 0; j0 < nk; j0 += U) {
-    uint4 raw[U][CH];
-    int64_t rows_[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int j = j0 + u;
-      rows_[u] = j < nk ? decode_key_row(a, c, r, j) : 0;
-      if (j < nk) {
-        const T* kr = kb + rows_[u] * a.ldkv;
-#pragma unroll
-        for (int ch = 0; ch < CH; ++ch)
-          raw[u][ch] = *reinterpret_cast<const uint4*>(kr + (lane + ch * 32) * VEC);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int j = j0 + u;
-      float sacc = 0.f;
-      if (j < nk) {
-#pragma unroll
-        for (int ch = 0; ch < CH; ++ch) {
-          float f[VEC];
-          cvt16<T>(raw[u][ch], f);
-#pragma unroll
-          for (int i = 0; i < VEC; ++i) sacc = fmaf(qf[ch][i], f[i], sacc);
-        }
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
-      if (j < nk) {
-        if (a.kc_off >= 0) sacc += qscale * to_f32(kb[rows_[u] * a.ldkv + a.kc_off]);
-        if (c.all_masked) sacc += kMaskValue;
-        if (lane == 0) S[j] = sacc;
-        mx = fmaxf(mx, sacc);
-      }
-    }
-  }
-  __syncwarp();
-  float sum = 0.f;
-  for (int j = lane; j < nk; j += 32) {
-    const float e = expf(S[j] - mx);
-    S[j] = e;
-    sum += e;
-  }
-  sum = warp_sum(sum);
-  for (int j = lane; j < nk; j += 32) S[j] = S[j] / sum;
-  __syncwarp();
-  float acc[CH][VEC];
-#pragma unroll
-  for (int ch = 0; ch < CH; ++ch)
-#pragma unroll
-    for (int i = 0; i < VEC; ++i) acc[ch][i] = 0.f;
-  for (int j0 = 0; j0 < nk; j0 += U) {
-    uint4 raw[U][CH];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int j = j0 + u;
-      if (j < nk) {
-        const T* vr = vb + decode_key_row(a, c, r, j) * a.ldkv;
-#pragma unroll
-        for (int ch = 0; ch < CH; ++ch)
-          raw[u][ch] = *reinterpret_cast<const uint4*>(vr + (lane + ch * 32) * VEC);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int j = j0 + u;
-      if (j < nk) {
-        const float w = S[j];
-#pragma unroll
-        for (int ch = 0; ch < CH; ++ch) {
-          float f[VEC];
-          cvt16<T>(raw[u][ch], f);
-#pragma unroll
-          for (int i = 0; i < VEC; ++i) acc[ch][i] = fmaf(w, f[i], acc[ch][i]);
-        }
-      }
-    }
-  }
-#pragma unroll
-  for (int ch = 0; ch < CH; ++ch) {
-    const int e0 = (lane + ch * 32) * VEC;
-    if (a.out_f32) {
-      float* out = reinterpret_cast<float*>(a.out) + (size_t)r * a.ldo + e0;
-#pragma unroll
-      for (int i = 0; i < VEC; ++i) out[i] = a.out_bias ? acc[ch][i] + a.out_bias[e0 + i] : acc[ch][i];
-    } else {
-      T* out = reinterpret_cast<T*>(a.out) + (size_t)r * a.ldo + e0;
-#pragma unroll
-      for (int i = 0; i < VEC; ++i) out[i] = from_f32<T>(acc[ch][i]);
-    }
-  }
-}
-
-bool dec_warp_enabled() {
-  static int on = -1;
-  if (on < 0) {
-    const char* e = getenv("FNMT_DEC_WARP");
-    on = !(e && e[0] == '0');
-  }
-  return on != 0;
-}
-
-template <typename T>
-cudaError_t try_dec_warp(const DecAttnArgs& a, float qscale, cudaStream_t s) {
-  constexpr int VEC = Vec16<T>::N;
-  constexpr int WPC = 4;
-  if (sizeof(T) != 2 || a.heads != 1 || !dec_warp_enabled() || a.dk % (32 * VEC) ||
-      (a.ldkv % VEC) || (a.ldq % VEC) || a.ngain)
-    return cudaErrorNotSupported;
-  const size_t smem = sizeof(float) * (size_t)WPC * a.max_k;
-  if (smem > 227 * 1024) return cudaErrorNotSupported;
-  const dim3 grid((a.rows + WPC - 1) / WPC);
-  switch (a.dk / (32 * VEC)) {
-    case 1: {
-      auto k = attn_decode_warp_kernel<T, 1, 4, WPC>;
-      if (smem > 48 * 1024 && set_max_smem((const void*)k) != cudaSuccess) return cudaErrorInvalidValue;
-      return launch_k(k, grid, dim3(WPC * 32), smem, s, a, qscale);
-    }
-    case 2: {
-      auto k = attn_decode_warp_kernel<T, 2, 4, WPC>;
-      if (smem > 48 * 1024 && set_max_smem((const void*)k) != cudaSuccess) return cudaErrorInvalidValue;
-      return launch_k(k, grid, dim3(WPC * 32), smem, s, a, qscale);
-    }
-    default:
-      return cudaErrorNotSupported;
-  }
-}
-
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)),
                "l"(gmem_src)
@@ -1129,9 +943,7 @@ cudaError_t decode_dispatch(const DecAttnArgs& a, cudaStream_t s) {
   constexpr int VEC = Vec16<T>::N;
   const float qscale = (float)(1.0 / sqrt((double)a.dk));
   if constexpr (sizeof(T) == 2) {
-    cudaError_t e = try_dec_rows<T>(a, qscale, s);
-    if (e != cudaErrorNotSupported) return e;
-    e = try_dec_warp<T>(a, qscale, s);
+    const cudaError_t e = try_dec_rows<T>(a, qscale, s);
     if (e != cudaErrorNotSupported) return e;
   }
   const int nch = a.dk / VEC;

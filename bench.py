@@ -93,6 +93,8 @@ def reduce_max_sum(dist, world, device, t_max, x_sum):
     if world == 1:
         return t_max, x_sum
     import torch
+    if dist.get_backend() == "gloo":   # FNMT_DIST_BACKEND=gloo: CPU tensors
+        device = torch.device("cpu")
     a = torch.tensor([t_max], dtype=torch.float64, device=device)
     b = torch.tensor([x_sum], dtype=torch.float64, device=device)
     dist.all_reduce(a, op=dist.ReduceOp.MAX)
@@ -293,9 +295,14 @@ def main():
         return run_reference(args)
     import torch
     world, rank, local = dist_env()
+    # one GPU per rank; FNMT_DIST_BACKEND=gloo with fewer GPUs than ranks maps
+    # ranks onto the visible devices (a dry run of the N > 1 path on one GPU)
+    backend = os.environ.get("FNMT_DIST_BACKEND", "nccl")
+    if backend == "gloo":
+        local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
-    dist = dist_init(world, "nccl")
+    dist = dist_init(world, backend)
 
     from paper_2109_08003_b200 import store as S
     from paper_2109_08003_b200.engine import Engine, budgets_of

@@ -68,6 +68,9 @@ def parse():
     ap.add_argument("--sbatch", type=int, default=3072, help="sentence cap (paper GPU setting 3072)")
     ap.add_argument("--model", choices=sorted(MODELS), default="6-1-1")
     ap.add_argument("--beam", type=int, default=1)
+    ap.add_argument("--sim-rank", type=int, default=None,
+                    help="debug: run rank R's chunk sequence of a --sim-world job in one process")
+    ap.add_argument("--sim-world", type=int, default=1)
     return ap.parse_args()
 
 
@@ -335,8 +338,10 @@ def main():
     d_out_len = torch.zeros((max(K, 1), C), dtype=torch.int32, device=device)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)
 
+    crank, cworld = (args.sim_rank, args.sim_world) if args.sim_rank is not None else (rank, world)
+
     def chunk_of(i):
-        return (rank + i * world) % n_chunks
+        return (crank + i * cworld) % n_chunks
 
     def device_step(c, slot):
         lo, hi, L, b, off = chunk_meta[c]

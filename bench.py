@@ -383,6 +383,7 @@ def main():
 
     # ---- e2e: public host-buffer API, H2D + D2H inside each step -------------
     pin_ids = torch.from_numpy(ids).pin_memory()
+    pin_ids_np = pin_ids.numpy()
     pin_out = torch.empty(max_out, dtype=torch.int32).pin_memory()
     pin_len = torch.empty(C, dtype=torch.int32).pin_memory()
     h2d = d2h = 0
@@ -390,7 +391,9 @@ def main():
     def host_step(c):
         lo, hi, L, b, off = chunk_meta[c]
         n_ids = int(offsets[hi] - offsets[lo])
-        eng.translate(pin_ids[int(offsets[lo]):int(offsets[hi])].numpy(), offsets[lo:hi + 1],
+        # the C ABI reads sentence i at ids[offsets[i]:offsets[i+1]] (absolute
+        # offsets into the corpus array, rebased on the device): pass the base
+        eng.translate(pin_ids_np, offsets[lo:hi + 1],
                       sbatch=SBATCH, wbatch=WBATCH, out_ids=pin_out.numpy(),
                       out_len=pin_len.numpy(), out_off=off, beam=BEAM)
         return n_ids * 4 + (hi - lo + 1) * 8 + (hi - lo) * 8, int(b.sum()) * 4 + (hi - lo) * 4
@@ -417,7 +420,9 @@ def main():
     e_el = e0.elapsed_time(e1) / 1e3
     e_max, e_words_all = reduce_max_sum(dist, world, device, e_el, float(e2e_words))
     e2e = {"value": e_words_all / e_max, "unit": UNIT, "h2d_bytes_per_step": h2d // max(K, 1),
-           "d2h_bytes_per_step": d2h // max(K, 1)}
+           "d2h_bytes_per_step": d2h // max(K, 1),
+           # same chunks through both paths: the word counts must agree exactly
+           "matches_device_path": bool(e2e_words == int(words))}
 
     peak_alloc = torch.cuda.max_memory_allocated(device)
     engine_bytes = eng.device_bytes()

@@ -265,3 +265,23 @@ def test_fold_norm_path():
                        env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "fold norm ok" in r.stdout
+
+
+def test_engine_translate_absolute_offsets(golden):
+    """fnmt_engine_translate reads sentence i at ids[offsets[i]:offsets[i+1]]
+    with absolute offsets into the caller's array (include/fnmt_b200.h): a
+    slice of a corpus passed with its absolute offsets equals the rebased call."""
+    cfg, w, get = case(golden, "d32_student")
+    eng = Engine(cfg, w, dtype="f16")
+    rng = np.random.default_rng(3)
+    rows = [rng.integers(4, cfg.vocab_size, size=int(rng.integers(1, 20))) for _ in range(60)]
+    lengths = np.array([len(r) for r in rows])
+    offsets = np.concatenate([[0], np.cumsum(lengths)]).astype(np.int64)
+    ids = np.concatenate(rows).astype(np.int32)
+    lo, hi = 25, 60
+    a, alen, aoff, _ = eng.translate(ids, offsets[lo:hi + 1])
+    b, blen, boff, _ = eng.translate(ids[offsets[lo]:offsets[hi]].copy(),
+                                     offsets[lo:hi + 1] - offsets[lo])
+    assert split_off(a, alen, aoff) == split_off(b, blen, boff)
+    full, flen, foff, _ = eng.translate(ids, offsets)
+    assert split_off(full, flen, foff)[lo:hi] == split_off(a, alen, aoff)

@@ -39,7 +39,9 @@ import numpy as np
 from . import modelfile
 from .store import ModelConfig, config_of
 from .textpipe import (BOS_ID, EOS_ID, PAD_ID, BpeCodec, ChunkFailure, Vocabulary, bpe_decode,
-                       bpe_encode, detokenize, tokenize)
+                       bpe_encode, clean_line, detokenize, tokenize_word)
+
+_WORD_CACHE_MAX = 1 << 20
 
 PRECISIONS = ("f32", "f16", "bf16", "int8")
 HARD_SPLIT = 1024            # SPEC.md:369 default hard limit (BPE tokens)
@@ -91,6 +93,7 @@ class Translator:
             raise ValueError(f"vocabulary has {len(vocab)} entries, config says "
                              f"{self.cfg.vocab_size}")
         self.vocab = vocab
+        self._word_ids = {False: {}, True: {}}   # per pretokenized flag: word -> ids
         self.codec = codec
         self.run = run
         self.weights = weights
@@ -118,17 +121,42 @@ class Translator:
         t.run = new
         return t
 
+    @property
+    def codec(self) -> Optional[BpeCodec]:
+        return self._codec
+
+    @codec.setter
+    def codec(self, value: Optional[BpeCodec]) -> None:   # assignable, like the reference's
+        self._codec = value
+        self._word_ids = {False: {}, True: {}}
+
     # ---- host stages -------------------------------------------------------
+    def _word(self, word: str, pretok: bool) -> tuple:
+        toks = [word] if pretok else tokenize_word(word)
+        if self._codec is not None:
+            toks = bpe_encode(toks, self._codec)
+        return tuple(self.vocab.encode(toks))
+
     def _to_ids(self, lines: Sequence[str]) -> _Chunk:
+        """tokenize -> BPE -> vocab ids.  All three stages act word by word
+        (textpipe.tokenize splits the cleaned line on whitespace first), so the
+        ids of each distinct word are memoised: a Zipfian corpus turns into
+        dict lookups after its first few thousand lines."""
         pieces, owner = [], []
-        enc = self.vocab.encode
+        pretok = self.run.pretokenized
+        cache = self._word_ids[pretok]
         for li, line in enumerate(lines):
-            toks = line.split() if self.run.pretokenized else tokenize(line)
-            if self.codec is not None:
-                toks = bpe_encode(toks, self.codec)
-            ids = np.asarray(enc(toks), dtype=np.int32)
-            for s in range(0, len(ids), self.limit):
-                pieces.append(ids[s:s + self.limit])
+            ids: list = []
+            for w in (line.split() if pretok else clean_line(line).split()):
+                t = cache.get(w)
+                if t is None:
+                    t = self._word(w, pretok)
+                    if len(cache) < _WORD_CACHE_MAX:
+                        cache[w] = t
+                ids.extend(t)
+            arr = np.asarray(ids, dtype=np.int32)
+            for s in range(0, len(arr), self.limit):
+                pieces.append(arr[s:s + self.limit])
                 owner.append(li)
         return _Chunk(pieces, owner, len(lines))
 
@@ -139,7 +167,7 @@ class Translator:
             per_line[li].extend(tok(int(i)) for i in ids)
         res = []
         for sub in per_line:
-            words = bpe_decode(sub) if self.codec is not None else sub
+            words = bpe_decode(sub) if self._codec is not None else sub
             res.append(" ".join(words) if self.run.pretokenized else detokenize(words))
         return res
 

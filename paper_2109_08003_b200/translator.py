@@ -29,8 +29,9 @@ cap-invariance contracts, test_engine_cli.py:39-55).
 
 from __future__ import annotations
 
+import multiprocessing as mp
 import time
-from concurrent.futures import ThreadPoolExecutor
+from concurrent.futures import ProcessPoolExecutor, ThreadPoolExecutor
 from dataclasses import dataclass, replace
 from typing import Optional, Sequence
 
@@ -77,6 +78,25 @@ class RunConfig:
         object.__setattr__(self, "devices", tuple(int(d) for d in self.devices))
 
 
+# Text stages in forked worker processes (run.workers > 1): pure-Python
+# tokenize / BPE / detokenize are GIL-bound, so threads do not scale; the
+# workers inherit the Translator (vocabulary, codec, word caches) at fork time
+# and never touch CUDA.
+_FORK_TEXT = None
+
+
+def _proc_ready(_):
+    return True
+
+
+def _proc_to_ids(lines, pretok):
+    return _FORK_TEXT._to_ids(lines, pretok)
+
+
+def _proc_to_text(chunk, outs, pretok):
+    return _FORK_TEXT._to_text(chunk, outs, pretok)
+
+
 @dataclass
 class _Chunk:
     pieces: list          # list[np.ndarray int32] subword ids, each <= limit
@@ -94,6 +114,7 @@ class Translator:
                              f"{self.cfg.vocab_size}")
         self.vocab = vocab
         self._word_ids = {False: {}, True: {}}   # per pretokenized flag: word -> ids
+        self._pools: dict = {}                   # workers -> forked text-stage pool
         self.codec = codec
         self.run = run
         self.weights = weights
@@ -129,6 +150,32 @@ class Translator:
     def codec(self, value: Optional[BpeCodec]) -> None:   # assignable, like the reference's
         self._codec = value
         self._word_ids = {False: {}, True: {}}
+        self.close_pools()   # forked workers hold the old codec
+
+    def close_pools(self) -> None:
+        for pool in getattr(self, "_pools", {}).values():
+            pool.shutdown(wait=False, cancel_futures=True)
+        if hasattr(self, "_pools"):
+            self._pools.clear()
+
+    def __del__(self):
+        try:
+            self.close_pools()
+        except Exception:   # noqa: BLE001 - interpreter teardown
+            pass
+
+    def _proc_pool(self):
+        """The forked text-stage pool for run.workers (created once, workers
+        started eagerly so the fork happens here, outside any engine call)."""
+        global _FORK_TEXT
+        n = self.run.workers
+        pool = self._pools.get(n)
+        if pool is None:
+            _FORK_TEXT = self
+            pool = ProcessPoolExecutor(max_workers=n, mp_context=mp.get_context("fork"))
+            list(pool.map(_proc_ready, range(n)))
+            self._pools[n] = pool
+        return pool
 
     # ---- host stages -------------------------------------------------------
     def _word(self, word: str, pretok: bool) -> tuple:
@@ -137,13 +184,13 @@ class Translator:
             toks = bpe_encode(toks, self._codec)
         return tuple(self.vocab.encode(toks))
 
-    def _to_ids(self, lines: Sequence[str]) -> _Chunk:
+    def _to_ids(self, lines: Sequence[str], pretok: Optional[bool] = None) -> _Chunk:
         """tokenize -> BPE -> vocab ids.  All three stages act word by word
         (textpipe.tokenize splits the cleaned line on whitespace first), so the
         ids of each distinct word are memoised: a Zipfian corpus turns into
         dict lookups after its first few thousand lines."""
         pieces, owner = [], []
-        pretok = self.run.pretokenized
+        pretok = self.run.pretokenized if pretok is None else pretok
         cache = self._word_ids[pretok]
         for li, line in enumerate(lines):
             ids: list = []
@@ -160,7 +207,8 @@ class Translator:
                 owner.append(li)
         return _Chunk(pieces, owner, len(lines))
 
-    def _to_text(self, chunk: _Chunk, outs: list) -> list:
+    def _to_text(self, chunk: _Chunk, outs: list, pretok: Optional[bool] = None) -> list:
+        pretok = self.run.pretokenized if pretok is None else pretok
         per_line = [[] for _ in range(chunk.n_lines)]
         tok = self.vocab.token_of
         for li, ids in zip(chunk.owner, outs):
@@ -168,7 +216,7 @@ class Translator:
         res = []
         for sub in per_line:
             words = bpe_decode(sub) if self._codec is not None else sub
-            res.append(" ".join(words) if self.run.pretokenized else detokenize(words))
+            res.append(" ".join(words) if pretok else detokenize(words))
         return res
 
     # ---- GPU stage -----------------------------------------------------------
@@ -208,9 +256,15 @@ class Translator:
         groups = self._groups(len(lines))
         n_eng = len(self.engines)
         posted: list = [None] * len(groups)     # per group: futures of detokenized chunks
-        with ThreadPoolExecutor(max_workers=self.run.workers) as pool:
+        pretok = self.run.pretokenized
+        procs = self.run.workers > 1
+        with ThreadPoolExecutor(max_workers=1 if procs else self.run.workers) as tpool:
+            pool = self._proc_pool() if procs else tpool
+            pre_fn = _proc_to_ids if procs else self._to_ids
+            post_fn = _proc_to_text if procs else self._to_text
+
             def prep(gi):
-                return [pool.submit(self._to_ids, lines[s:e]) for s, e in groups[gi]]
+                return [pool.submit(pre_fn, lines[s:e], pretok) for s, e in groups[gi]]
 
             def lane(e):
                 mine = list(range(e, len(groups), n_eng))
@@ -226,7 +280,7 @@ class Translator:
                                                  self.engines[e])
                     futs, o = [], 0
                     for c in chunks:
-                        futs.append(pool.submit(self._to_text, c, res[o:o + len(c.pieces)]))
+                        futs.append(pool.submit(post_fn, c, res[o:o + len(c.pieces)], pretok))
                         o += len(c.pieces)
                     posted[gi] = futs
 

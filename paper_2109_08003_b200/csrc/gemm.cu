@@ -378,8 +378,10 @@ __device__ __forceinline__ void norm_epilogue(const EpiParams& ep, uint32_t tadd
 // persistent tcgen05 kernel
 
 // Every stage row is 128 bytes of K: 64 fp16/bf16 elements, or 128 int8.
-template <int BN, int STAGES, bool I8 = false, int CN = 0>
+template <int BN, int STAGES, bool I8 = false, int CN = 0, int TK = 0>
 struct TcCfg {
+  // TK (beam top-K epilogue): per-row exchange of the two column halves' partials
+  static constexpr int kTkBytes = TK ? kBM * (4 + 8 + 8 * TK) : 0;
   static constexpr int kBKe = I8 ? 2 * kBK : kBK;   // K elements per stage
   static constexpr int kBBytes = BN * kBK * 2;
   static constexpr int kStage = kABytes + kBBytes;
@@ -387,7 +389,8 @@ struct TcCfg {
   static constexpr int kColBytes = I8 ? 16 : 4;   // bias (+ scale, zeropoint, column sum)
   // kEpiNorm: row-statistic slots [parity][pass][rank][128] + half-row partials [2][128]
   static constexpr int kNormBytes = CN ? (4 * CN * kBM + 2 * kBM) * 8 + 64 : 0;
-  static constexpr int kSmem = 1024 + STAGES * kStage + 2 * BN * kColBytes + kNormBytes + 256;
+  static constexpr int kSmem =
+      1024 + STAGES * kStage + 2 * BN * kColBytes + kNormBytes + kTkBytes + 256;
 };
 
 // Tile of this CTA's it-th iteration (-1 when done).  Plain: a grid-stride
@@ -406,14 +409,18 @@ __device__ __forceinline__ int tile_at(int it, int tiles, int tiles_n) {
 }
 
 
-// Beam epilogue for one row of one 128-column half tile (kTopKTile): two
-// passes over the TMEM accumulator (max + running top-K, then sum of
-// exp(x - max)); the partials are merged per row by beam_row_reduce (beam.cu).
-// `taddr`/`bs`/`n0` point at the first column of this warp's half.
+// Beam epilogue for one row of a 256-column tile (kTopKTile): each of the two
+// warps of a TMEM lane quarter makes two passes over its 128-column half (max
+// + running top-K, then sum of exp(x - max)); the half-1 warp hands its
+// partial to the half-0 warp through shared memory, which merges them (max,
+// rescaled sum, top-K in (value desc, index asc) order — half 0 holds the
+// lower indices, so a strict '>' keeps ties on the lower id) and writes one
+// partial per (row, tile) for beam_row_reduce (beam.cu).
 template <int BN, int TOPK>
 __device__ __forceinline__ void topk_epilogue(const EpiParams& ep, uint32_t taddr, const float* bs,
-                                              int m, bool row_ok, int n0) {
-  static_assert(BN / 2 == kTopKTile, "half tile == top-K partial tile");
+                                              int m, bool row_ok, int n0, int half, int row,
+                                              uint8_t* scratch) {
+  static_assert(BN == kTopKTile, "a 256-column tile per top-K partial");
   float mx = -INFINITY;
   float tv[TOPK];
   int ti[TOPK];
@@ -464,10 +471,49 @@ __device__ __forceinline__ void topk_epilogue(const EpiParams& ep, uint32_t tadd
     }
     sum += (double)cs;
   }
-  if (row_ok && n0 < ep.N) {   // a half tile entirely past N has no partial slot
+  float* smx = reinterpret_cast<float*>(scratch);                 // [kBM]
+  double* ssum = reinterpret_cast<double*>(scratch + 4 * kBM);     // [kBM]
+  float* stv = reinterpret_cast<float*>(scratch + 12 * kBM);       // [TOPK][kBM]
+  int* sti = reinterpret_cast<int*>(scratch + (12 + 4 * TOPK) * kBM);
+  if (half == 1) {
+    smx[row] = mx;
+    ssum[row] = sum;
+#pragma unroll
+    for (int j = 0; j < TOPK; ++j) {
+      stv[j * kBM + row] = tv[j];
+      sti[j * kBM + row] = ti[j];
+    }
+  }
+  named_bar_sync(1, kEpiWarps * 32);
+  if (half != 0) return;
+  const float m1 = smx[row];
+  const float M = fmaxf(mx, m1);
+  double tot = 0.0;
+  if (mx > -INFINITY) tot += sum * exp((double)mx - (double)M);
+  if (m1 > -INFINITY) tot += ssum[row] * exp((double)m1 - (double)M);
+#pragma unroll
+  for (int k = 0; k < TOPK; ++k) {
+    const float x = stv[k * kBM + row];
+    if (x > tv[TOPK - 1]) {
+      tv[TOPK - 1] = x;
+      ti[TOPK - 1] = sti[k * kBM + row];
+#pragma unroll
+      for (int j = TOPK - 1; j > 0; --j) {
+        if (tv[j] > tv[j - 1]) {
+          const float fv = tv[j];
+          tv[j] = tv[j - 1];
+          tv[j - 1] = fv;
+          const int iv = ti[j];
+          ti[j] = ti[j - 1];
+          ti[j - 1] = iv;
+        }
+      }
+    }
+  }
+  if (row_ok && n0 < ep.N) {
     const size_t o = (size_t)m * ep.tk.tiles + n0 / kTopKTile;
-    ep.tk.pmax[o] = mx;
-    ep.tk.psum[o] = sum;
+    ep.tk.pmax[o] = M;
+    ep.tk.psum[o] = tot;
 #pragma unroll
     for (int j = 0; j < TOPK; ++j) {
       ep.tk.pval[o * TOPK + j] = tv[j];
@@ -480,7 +526,7 @@ template <int BN, int STAGES, int TOPK, bool I8 = false, int MINB = 1, int CN = 
 __global__ void __launch_bounds__(kTcThreads, MINB)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmw,
                    int K, uint32_t idesc, EpiParams ep, int tiles_n, int tiles) {
-  using Cfg = TcCfg<BN, STAGES, I8, CN>;
+  using Cfg = TcCfg<BN, STAGES, I8, CN, TOPK>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -495,7 +541,8 @@ __global__ void __launch_bounds__(kTcThreads, MINB)
   double* nslot = reinterpret_cast<double*>(bias_s + (Cfg::kColBytes / 4) * 2 * BN);
   double* nhalf = nslot + (CN ? 4 * CN * kBM : 0);
   uint64_t* nbar = reinterpret_cast<uint64_t*>(nhalf + (CN ? 2 * kBM : 0));   // [parity][pass]
-  uint64_t* full = nbar + (CN ? 4 : 0);
+  uint8_t* tks = reinterpret_cast<uint8_t*>(nbar + (CN ? 4 : 0));   // TOPK: half exchange
+  uint64_t* full = reinterpret_cast<uint64_t*>(tks + Cfg::kTkBytes);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
@@ -627,7 +674,8 @@ __global__ void __launch_bounds__(kTcThreads, MINB)
         __syncwarp();
         if (lane == 0) mbar_arrive(tempty + acc);
       } else if constexpr (TOPK > 0) {
-        topk_epilogue<BN, TOPK>(ep, taddr, bs + col0, m, row_ok, n0 + col0);
+        topk_epilogue<BN, TOPK>(ep, taddr, bs + col0, m, row_ok, n0 + col0, half,
+                                quarter * 32 + lane, tks);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(tempty + acc);
@@ -753,7 +801,7 @@ int num_sms() {
 template <int BN, int STAGES, int TOPK = 0, bool I8 = false, int MINB = 1>
 cudaError_t launch_tc(const CUtensorMap& ta, const CUtensorMap& tw, const GemmArgs& g,
                       const EpiParams& ep, cudaStream_t s) {
-  using Cfg = TcCfg<BN, STAGES, I8>;
+  using Cfg = TcCfg<BN, STAGES, I8, 0, TOPK>;
   static_assert(Cfg::kSmem <= 227 * 1024, "GEMM stage ring exceeds shared memory");
   static_assert(MINB == 1 || MINB * (Cfg::kSmem + 1024) <= 228 * 1024, "MINB CTAs do not fit");
   auto kern = gemm_tc_kernel<BN, STAGES, TOPK, I8, MINB>;
@@ -1155,7 +1203,7 @@ cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t s) {
     }
   }
   if (g.epi == kEpiTopK) {
-    static_assert(kTopKTile == 128, "top-K partial tiles are half of BN = 256");
+    static_assert(kTopKTile == 256, "one top-K partial per BN = 256 tile");
     return g.topk.K == 4 ? launch_tc<256, 4, 4>(*pa, *pw, g, ep, s)
                          : launch_tc<256, 4, 8>(*pa, *pw, g, ep, s);
   }

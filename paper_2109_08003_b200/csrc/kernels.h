@@ -60,7 +60,7 @@ enum Epilogue : int {
 };
 
 // Per-(row, N-tile) partials of the beam epilogue; tile = n / kTopKTile.
-constexpr int kTopKTile = 128;
+constexpr int kTopKTile = 256;   // one partial per (row, 256-column GEMM tile)
 constexpr int kTopKMax = 8;
 struct TopKPartials {
   float* pmax;     // [rows][tiles]

@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(kMThreads)
   float* S = reinterpret_cast<float*>(smraw);          // [kMQ][scap] fp32 scores / probabilities
   T* Qs = reinterpret_cast<T*>(S + kMQ * scap);        // [kMQ][kLds]
   T* Ks = Qs + kMQ * kLds;                             // [kMK][kLds]  (V tile in phase 3)
-  const int b = blockIdx.y;
+  const int b = blockIdx.y, h = blockIdx.z;
   const int q0 = blockIdx.x * kMQ;
   const int nq = a.q_len[b];
   if (q0 >= nq) return;
@@ -119,129 +119,126 @@ __global__ void __launch_bounds__(kMThreads)
   const int64_t qrow0 = a.q_start[b] + q0;
   const int64_t krow0 = a.k_start[b];
   const int dk = a.dk;
-  // heads h = blockIdx.z, blockIdx.z + gridDim.z, ...: small heads share a CTA
-  for (int h = blockIdx.z; h < a.heads; h += gridDim.z) {
-    const T* q = reinterpret_cast<const T*>(a.q) + h * dk;
-    const T* k = reinterpret_cast<const T*>(a.k) + h * dk;
-    const T* v = reinterpret_cast<const T*>(a.v) + h * dk;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int g = lane >> 2, tig = lane & 3;
-    const int wr = warp * 16;
-    const bool live = wr < qn;
+  const T* q = reinterpret_cast<const T*>(a.q) + h * dk;
+  const T* k = reinterpret_cast<const T*>(a.k) + h * dk;
+  const T* v = reinterpret_cast<const T*>(a.v) + h * dk;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, tig = lane & 3;
+  const int wr = warp * 16;
+  const bool live = wr < qn;
 
-    // ---- 1. scores ------------------------------------------------------------
-    for (int kt = 0; kt < nk; kt += kMK) {
-      float acc[8][4];
+  // ---- 1. scores ------------------------------------------------------------
+  for (int kt = 0; kt < nk; kt += kMK) {
+    float acc[8][4];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
-      for (int dc = 0; dc < dk; dc += kMD) {
-        __syncthreads();
-        stage_tile(Qs, q, qrow0, a.ldq, qn, dc, dk);
-        stage_tile(Ks, k, krow0 + kt, a.ldkv, nk - kt, dc, dk);
-        __syncthreads();
-        if (live) {
-#pragma unroll
-          for (int kk = 0; kk < kMD; kk += 16) {
-            uint32_t af[4];
-            const T* qa = Qs + (wr + g) * kLds + kk + 2 * tig;
-            af[0] = lds32(qa);
-            af[1] = lds32(qa + 8 * kLds);
-            af[2] = lds32(qa + 8);
-            af[3] = lds32(qa + 8 * kLds + 8);
-#pragma unroll
-            for (int nt = 0; nt < 8; ++nt) {
-              const T* kb = Ks + (nt * 8 + g) * kLds + kk + 2 * tig;
-              mma16816<T>(acc[nt], af, lds32(kb), lds32(kb + 8));
-            }
-          }
-        }
-      }
-      if (live) {
-#pragma unroll
-        for (int nt = 0; nt < 8; ++nt)
-#pragma unroll
-          for (int hh = 0; hh < 2; ++hh) {
-            const int qi = wr + g + 8 * hh;
-            const int kj = kt + nt * 8 + 2 * tig;
-            float s0 = acc[nt][2 * hh] * qscale, s1 = acc[nt][2 * hh + 1] * qscale;
-            if (all_masked) {
-              s0 += kMaskValue;
-              s1 += kMaskValue;
-            }
-            *reinterpret_cast<float2*>(S + qi * scap + kj) = make_float2(s0, s1);
-          }
-      }
-    }
-    __syncthreads();
-
-    // ---- 2. softmax (tensor.py:70-81), zero past nk / qn ------------------------
-    for (int qi = warp; qi < kMQ; qi += kMThreads / 32) {
-      float* pr = S + qi * scap;
-      if (qi >= qn) {
-        if (qi < ((qn + 15) & ~15))
-          for (int j = lane; j < scap; j += 32) pr[j] = 0.f;
-        continue;
-      }
-      float mx = -INFINITY;
-      for (int j = lane; j < nk; j += 32) mx = fmaxf(mx, pr[j]);
-      mx = warp_max(mx);
-      float sum = 0.f;
-      for (int j = lane; j < nk; j += 32) {
-        const float e = expf(pr[j] - mx);
-        pr[j] = e;
-        sum += e;
-      }
-      sum = warp_sum(sum);
-      for (int j = lane; j < nk; j += 32) pr[j] = pr[j] / sum;
-      for (int j = nk + lane; j < scap; j += 32) pr[j] = 0.f;
-    }
-
-    // ---- 3. O = P V ----------------------------------------------------------------
-    T* out = reinterpret_cast<T*>(a.out) + h * dk;
+    for (int i = 0; i < 8; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
     for (int dc = 0; dc < dk; dc += kMD) {
-      float o[8][4];
+      __syncthreads();
+      stage_tile(Qs, q, qrow0, a.ldq, qn, dc, dk);
+      stage_tile(Ks, k, krow0 + kt, a.ldkv, nk - kt, dc, dk);
+      __syncthreads();
+      if (live) {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
-      for (int kc = 0; kc < nk; kc += kMK) {
-        __syncthreads();
-        stage_tile(Ks, v, krow0 + kc, a.ldkv, nk - kc, dc, dk);
-        __syncthreads();
-        if (live) {
+        for (int kk = 0; kk < kMD; kk += 16) {
+          uint32_t af[4];
+          const T* qa = Qs + (wr + g) * kLds + kk + 2 * tig;
+          af[0] = lds32(qa);
+          af[1] = lds32(qa + 8 * kLds);
+          af[2] = lds32(qa + 8);
+          af[3] = lds32(qa + 8 * kLds + 8);
 #pragma unroll
-          for (int kk = 0; kk < kMK; kk += 16) {
-            const float* p0 = S + (wr + g) * scap + kc + kk + 2 * tig;
-            const float* p1 = p0 + 8 * scap;
-            uint32_t af[4];
-            af[0] = pack2<T>(p0[0], p0[1]);
-            af[1] = pack2<T>(p1[0], p1[1]);
-            af[2] = pack2<T>(p0[8], p0[9]);
-            af[3] = pack2<T>(p1[8], p1[9]);
-            // thread t addresses row (t & 7) of 8x8 matrix t >> 3:
-            // m0 keys kk..+7 / dims n0..+7, m1 keys +8, m2 dims +8, m3 both
-            const int mi = lane >> 3;
-            const int key = kk + (lane & 7) + ((mi & 1) ? 8 : 0);
-#pragma unroll
-            for (int nt = 0; nt < 8; nt += 2) {
-              uint32_t bf[4];
-              ldmatrix_x4_trans(bf, Ks + key * kLds + nt * 8 + ((mi & 2) ? 8 : 0));
-              mma16816<T>(o[nt], af, bf[0], bf[1]);
-              mma16816<T>(o[nt + 1], af, bf[2], bf[3]);
-            }
+          for (int nt = 0; nt < 8; ++nt) {
+            const T* kb = Ks + (nt * 8 + g) * kLds + kk + 2 * tig;
+            mma16816<T>(acc[nt], af, lds32(kb), lds32(kb + 8));
           }
         }
       }
+    }
+    if (live) {
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const int qi = wr + g + 8 * hh;
+          const int kj = kt + nt * 8 + 2 * tig;
+          float s0 = acc[nt][2 * hh] * qscale, s1 = acc[nt][2 * hh + 1] * qscale;
+          if (all_masked) {
+            s0 += kMaskValue;
+            s1 += kMaskValue;
+          }
+          *reinterpret_cast<float2*>(S + qi * scap + kj) = make_float2(s0, s1);
+        }
+    }
+  }
+  __syncthreads();
+
+  // ---- 2. softmax (tensor.py:70-81), zero past nk / qn ------------------------
+  for (int qi = warp; qi < kMQ; qi += kMThreads / 32) {
+    float* pr = S + qi * scap;
+    if (qi >= qn) {
+      if (qi < ((qn + 15) & ~15))
+        for (int j = lane; j < scap; j += 32) pr[j] = 0.f;
+      continue;
+    }
+    float mx = -INFINITY;
+    for (int j = lane; j < nk; j += 32) mx = fmaxf(mx, pr[j]);
+    mx = warp_max(mx);
+    float sum = 0.f;
+    for (int j = lane; j < nk; j += 32) {
+      const float e = expf(pr[j] - mx);
+      pr[j] = e;
+      sum += e;
+    }
+    sum = warp_sum(sum);
+    for (int j = lane; j < nk; j += 32) pr[j] = pr[j] / sum;
+    for (int j = nk + lane; j < scap; j += 32) pr[j] = 0.f;
+  }
+
+  // ---- 3. O = P V ----------------------------------------------------------------
+  T* out = reinterpret_cast<T*>(a.out) + h * dk;
+  for (int dc = 0; dc < dk; dc += kMD) {
+    float o[8][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+    for (int kc = 0; kc < nk; kc += kMK) {
+      __syncthreads();
+      stage_tile(Ks, v, krow0 + kc, a.ldkv, nk - kc, dc, dk);
+      __syncthreads();
       if (live) {
 #pragma unroll
-        for (int nt = 0; nt < 8; ++nt)
+        for (int kk = 0; kk < kMK; kk += 16) {
+          const float* p0 = S + (wr + g) * scap + kc + kk + 2 * tig;
+          const float* p1 = p0 + 8 * scap;
+          uint32_t af[4];
+          af[0] = pack2<T>(p0[0], p0[1]);
+          af[1] = pack2<T>(p1[0], p1[1]);
+          af[2] = pack2<T>(p0[8], p0[9]);
+          af[3] = pack2<T>(p1[8], p1[9]);
+          // thread t addresses row (t & 7) of 8x8 matrix t >> 3:
+          // m0 keys kk..+7 / dims n0..+7, m1 keys +8, m2 dims +8, m3 both
+          const int mi = lane >> 3;
+          const int key = kk + (lane & 7) + ((mi & 1) ? 8 : 0);
 #pragma unroll
-          for (int hh = 0; hh < 2; ++hh) {
-            const int qi = wr + g + 8 * hh;
-            const int dd = dc + nt * 8 + 2 * tig;
-            if (qi < qn && dd < dk)
-              *reinterpret_cast<uint32_t*>(out + (qrow0 + qi) * a.ldo + dd) =
-                  pack2<T>(o[nt][2 * hh], o[nt][2 * hh + 1]);
+          for (int nt = 0; nt < 8; nt += 2) {
+            uint32_t bf[4];
+            ldmatrix_x4_trans(bf, Ks + key * kLds + nt * 8 + ((mi & 2) ? 8 : 0));
+            mma16816<T>(o[nt], af, bf[0], bf[1]);
+            mma16816<T>(o[nt + 1], af, bf[2], bf[3]);
           }
+        }
       }
+    }
+    if (live) {
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const int qi = wr + g + 8 * hh;
+          const int dd = dc + nt * 8 + 2 * tig;
+          if (qi < qn && dd < dk)
+            *reinterpret_cast<uint32_t*>(out + (qrow0 + qi) * a.ldo + dd) =
+                pack2<T>(o[nt][2 * hh], o[nt][2 * hh + 1]);
+        }
     }
   }
 }
@@ -252,16 +249,7 @@ cudaError_t mma_dispatch(const AttnArgs& a, cudaStream_t s) {
   const size_t smem = sizeof(float) * (size_t)kMQ * scap + sizeof(T) * 2 * (size_t)64 * kLds;
   cudaError_t e = set_max_smem((const void*)attn_varlen_mma_kernel<T>);
   if (e != cudaSuccess) return e;
-  // heads per CTA: dk <= 64 heads are tiny per sequence (newstest mean 24 tokens),
-  // so FNMT_ATTN_HPC (default 1) heads share one CTA to amortise its setup
-  static int hpc = -1;
-  if (hpc < 0) {
-    const char* e = getenv("FNMT_ATTN_HPC");
-    hpc = e ? atoi(e) : 1;
-    if (hpc < 1) hpc = 1;
-  }
-  const int per = a.dk <= 64 ? std::min(hpc, a.heads) : 1;
-  dim3 grid((a.max_q + kMQ - 1) / kMQ, a.n_seq, (a.heads + per - 1) / per);
+  dim3 grid((a.max_q + kMQ - 1) / kMQ, a.n_seq, a.heads);
   const float qscale = (float)(1.0 / sqrt((double)a.dk));
   attn_varlen_mma_kernel<T><<<grid, kMThreads, smem, s>>>(a, qscale, scap);
   return cudaGetLastError();

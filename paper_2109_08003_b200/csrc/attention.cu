@@ -479,7 +479,7 @@ __global__ void __launch_bounds__(NT) attn_decode_kernel(DecAttnArgs a, float qs
 // row.  Versus a CTA per (row, head) this loads 8x fewer, 8x larger key
 // vectors per CTA and runs 8x fewer CTAs.  Same two-pass numerics as
 // attn_decode_kernel.
-template <typename T, int CH, int NT, int LPH, int U = 2, int UV = 4, int RQ = 1>
+template <typename T, int CH, int NT, int LPH, int U = 2, int UV = 4>
 __global__ void __launch_bounds__(NT) attn_decode_rows_kernel(DecAttnArgs a, float qscale) {
   pdl_trigger();
   pdl_wait();
@@ -488,27 +488,21 @@ __global__ void __launch_bounds__(NT) attn_decode_rows_kernel(DecAttnArgs a, flo
   // group.  LPH 0 (head sizes that do not map to a power-of-two lane group,
   // e.g. dk 96): per-chunk partials go through shared memory and lane h sums
   // head h's chunks in order.
-  // RQ > 1 (beam cross attention): the RQ rows of one sentence share its
-  // encoder keys, so the CTA takes all of them and loads each key once.
   static_assert(LPH == 0 || LPH == 8 || LPH == 16 || LPH == 32, "lanes per head");
-  static_assert(RQ == 1 || LPH > 0, "row groups use the shuffle path");
   constexpr int NW = NT / 32;
   extern __shared__ float sm[];
   const int H = a.heads, dk = a.dk, d = H * dk;
-  float* qs = sm;                                  // [RQ][d]
-  float* S = qs + RQ * d;                          // [RQ][H][max_k]
-  float* red = S + (size_t)RQ * H * a.max_k + 4;   // [groups][RQ][d]
+  float* qs = sm;                  // [d]
+  float* S = qs + d;               // [H][max_k]
+  float* red = S + (size_t)H * a.max_k + 4;   // [groups][d]
   const int groups_v = NT / (d / VEC);
-  float* part = red + (size_t)groups_v * RQ * d;   // LPH 0: [NW][U][32 CH]
-  const int r0 = blockIdx.x * RQ;
+  float* part = red + (size_t)groups_v * d;    // LPH 0: [NW][U][32 CH]
+  const int r = blockIdx.x;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  DecCtx c = decode_setup<T>(a, r0, 0);
-  for (int hh = 1; hh < H && a.self_mode && a.new_k; ++hh) c = decode_setup<T>(a, r0, hh);  // append all heads
-  for (int e = tid; e < RQ * d; e += NT) {
-    const int rq = e / d;
-    qs[e] = to_f32(reinterpret_cast<const T*>(a.q)[(size_t)(r0 + rq) * a.ldq + (e - rq * d)]) *
-            qscale;
-  }
+  DecCtx c = decode_setup<T>(a, r, 0);
+  for (int hh = 1; hh < H && a.self_mode && a.new_k; ++hh) c = decode_setup<T>(a, r, hh);  // append all heads
+  const T* q = reinterpret_cast<const T*>(a.q) + (size_t)r * a.ldq;
+  for (int e = tid; e < d; e += NT) qs[e] = to_f32(q[e]) * qscale;
   __syncthreads();
 
   const T* kb = reinterpret_cast<const T*>(a.k);
@@ -518,7 +512,7 @@ __global__ void __launch_bounds__(NT) attn_decode_rows_kernel(DecAttnArgs a, flo
     for (int u = 0; u < U; ++u) {
       const int j = j0 + u * NW;
       if (j < c.nk) {
-        const T* kr = kb + decode_key_row(a, c, r0, j) * a.ldkv;
+        const T* kr = kb + decode_key_row(a, c, r, j) * a.ldkv;
 #pragma unroll
         for (int ch = 0; ch < CH; ++ch) {
           const int e0 = (lane + ch * 32) * VEC;
@@ -532,25 +526,22 @@ __global__ void __launch_bounds__(NT) attn_decode_rows_kernel(DecAttnArgs a, flo
 #pragma unroll
       for (int ch = 0; ch < CH; ++ch) {
         const int e0 = (lane + ch * 32) * VEC;
-        float f[VEC];
-        if (j < c.nk && e0 < d) cvt16<T>(raw[u][ch], f);
+        float sacc = 0.f;
+        if (j < c.nk && e0 < d) {
+          float f[VEC];
+          cvt16<T>(raw[u][ch], f);
 #pragma unroll
-        for (int rq = 0; rq < RQ; ++rq) {
-          float sacc = 0.f;
-          if (j < c.nk && e0 < d) {
+          for (int i = 0; i < VEC; ++i) sacc = fmaf(qs[e0 + i], f[i], sacc);
+        }
+        if constexpr (LPH > 0) {
 #pragma unroll
-            for (int i = 0; i < VEC; ++i) sacc = fmaf(qs[rq * d + e0 + i], f[i], sacc);
+          for (int o = LPH / 2; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
+          if ((lane % LPH) == 0 && j < c.nk && e0 < d) {
+            const int hh = e0 / dk;
+            S[(size_t)hh * a.max_k + j] = c.all_masked ? sacc + kMaskValue : sacc;
           }
-          if constexpr (LPH > 0) {
-#pragma unroll
-            for (int o = LPH / 2; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
-            if ((lane % LPH) == 0 && j < c.nk && e0 < d) {
-              const int hh = e0 / dk;
-              S[((size_t)rq * H + hh) * a.max_k + j] = c.all_masked ? sacc + kMaskValue : sacc;
-            }
-          } else {
-            part[(warp * U + u) * 32 * CH + lane + ch * 32] = sacc;
-          }
+        } else {
+          part[(warp * U + u) * 32 * CH + lane + ch * 32] = sacc;
         }
       }
     }
@@ -573,53 +564,46 @@ __global__ void __launch_bounds__(NT) attn_decode_rows_kernel(DecAttnArgs a, flo
     }
   }
   __syncthreads();
-  for (int hh = warp; hh < RQ * H; hh += NW) softmax_inplace(S + (size_t)hh * a.max_k, c.nk);
+  for (int hh = warp; hh < H; hh += NW) softmax_inplace(S + (size_t)hh * a.max_k, c.nk);
   __syncthreads();
 
   const int nch = d / VEC;
   const int groups = NT / nch;
   const int chn = tid % nch, grp = tid / nch;
   const T* vb = reinterpret_cast<const T*>(a.v) + chn * VEC;
-  const int head = (chn * VEC) / dk;
-  float acc[RQ][VEC];
+  const float* Sh = S + (size_t)((chn * VEC) / dk) * a.max_k;
+  float acc[VEC];
 #pragma unroll
-  for (int rq = 0; rq < RQ; ++rq)
-#pragma unroll
-    for (int i = 0; i < VEC; ++i) acc[rq][i] = 0.f;
+  for (int i = 0; i < VEC; ++i) acc[i] = 0.f;
   if (grp < groups) {
     for (int j0 = grp; j0 < c.nk; j0 += groups * UV) {
       uint4 rv[UV];
 #pragma unroll
       for (int u = 0; u < UV; ++u) {
         const int j = j0 + u * groups;
-        if (j < c.nk) rv[u] = *reinterpret_cast<const uint4*>(vb + decode_key_row(a, c, r0, j) * a.ldkv);
+        if (j < c.nk) rv[u] = *reinterpret_cast<const uint4*>(vb + decode_key_row(a, c, r, j) * a.ldkv);
       }
 #pragma unroll
       for (int u = 0; u < UV; ++u) {
         const int j = j0 + u * groups;
         if (j < c.nk) {
+          const float w = Sh[j];
           float f[VEC];
           cvt16<T>(rv[u], f);
 #pragma unroll
-          for (int rq = 0; rq < RQ; ++rq) {
-            const float w = S[((size_t)rq * H + head) * a.max_k + j];
-#pragma unroll
-            for (int i = 0; i < VEC; ++i) acc[rq][i] = fmaf(w, f[i], acc[rq][i]);
-          }
+          for (int i = 0; i < VEC; ++i) acc[i] = fmaf(w, f[i], acc[i]);
         }
       }
     }
 #pragma unroll
-    for (int rq = 0; rq < RQ; ++rq)
-#pragma unroll
-      for (int i = 0; i < VEC; ++i) red[((size_t)grp * RQ + rq) * d + chn * VEC + i] = acc[rq][i];
+    for (int i = 0; i < VEC; ++i) red[grp * d + chn * VEC + i] = acc[i];
   }
   __syncthreads();
-  for (int e = tid; e < RQ * d; e += NT) {
-    const int rq = e / d, ee = e - rq * d;
-    float sum = red[(size_t)rq * d + ee];
-    for (int gg = 1; gg < groups; ++gg) sum += red[((size_t)gg * RQ + rq) * d + ee];
-    reinterpret_cast<T*>(a.out)[(size_t)(r0 + rq) * a.ldo + ee] = from_f32<T>(sum);
+  T* out = reinterpret_cast<T*>(a.out) + (size_t)r * a.ldo;
+  for (int e = tid; e < d; e += NT) {
+    float sum = red[e];
+    for (int gg = 1; gg < groups; ++gg) sum += red[gg * d + e];
+    out[e] = from_f32<T>(sum);
   }
 }
 
@@ -906,39 +890,20 @@ bool dec_rows_enabled() {
   return on != 0;
 }
 
-bool dec_rows_beam_enabled() {
-  static int on = -1;
-  if (on < 0) {
-    const char* e = getenv("FNMT_DEC_ROWS_BEAM");
-    on = !(e && e[0] == '0');
-  }
-  return on != 0;
-}
-
-template <typename T, int CH, int LPH, int RQ = 1>
-cudaError_t launch_dec_rows_rq(const DecAttnArgs& a, float qscale, cudaStream_t s) {
+template <typename T, int CH, int LPH>
+cudaError_t launch_dec_rows(const DecAttnArgs& a, float qscale, cudaStream_t s) {
   constexpr int NT = 128;
   const int d = a.heads * a.dk;
   const int groups = NT / (d / Vec16<T>::N);
-  const size_t smem =
-      sizeof(float) * ((size_t)RQ * d + (size_t)RQ * a.heads * a.max_k + 4 +
-                       (size_t)groups * RQ * d + (LPH ? 0 : (NT / 32) * 2 * 32 * CH));
+  const size_t smem = sizeof(float) * ((size_t)d + (size_t)a.heads * a.max_k + 4 +
+                                       (size_t)groups * d + (LPH ? 0 : (NT / 32) * 2 * 32 * CH));
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
-  auto kern = attn_decode_rows_kernel<T, CH, NT, LPH, 2, 4, RQ>;
+  auto kern = attn_decode_rows_kernel<T, CH, NT, LPH>;
   if (smem > 48 * 1024) {
     cudaError_t e = set_max_smem((const void*)kern);
     if (e != cudaSuccess) return e;
   }
-  return launch_k(kern, dim3(a.rows / RQ), dim3(NT), smem, s, a, qscale);
-}
-
-template <typename T, int CH, int LPH>
-cudaError_t launch_dec_rows(const DecAttnArgs& a, float qscale, cudaStream_t s) {
-  if constexpr (LPH > 0) {   // beam cross attention: a sentence's 4 rows share its keys
-    if (!a.self_mode && a.rows_per_seq == 4 && a.rows % 4 == 0 && dec_rows_beam_enabled())
-      return launch_dec_rows_rq<T, CH, LPH, 4>(a, qscale, s);
-  }
-  return launch_dec_rows_rq<T, CH, LPH, 1>(a, qscale, s);
+  return launch_k(kern, dim3(a.rows), dim3(NT), smem, s, a, qscale);
 }
 
 // Multi-head rows: heads of 8 / 16 / 32 lanes (fp16 dk 64 / 128 / 256), a row of

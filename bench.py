@@ -167,67 +167,173 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------
-# CPU baseline: the oracle port (oracle/nmt_oracle.py) on the host cores
+# CPU baseline: the reference's own CPU path (baseline/_ref, the unmodified
+# fastnmt package, when installed; else the oracle port oracle/nmt_oracle.py,
+# pinned bit-exact to the reference) on the host cores.  One measurement
+# shared by both arms: a "CPU step" = every process translating PER_PROC
+# consecutive corpus sentences (one reference batch) with one thread
+# ("one MKL thread for each process").  Worker processes come
+# from a forkserver (never forked from the CUDA-initialised bench process).
 
-_CPU_STATE = {}
+REF_DIR = ROOT / "baseline" / "_ref"
+PER_PROC = 8
+_CPU = {}
+
+
+def reference_available() -> bool:
+    return (REF_DIR / "fastnmt" / "search.py").exists()
+
+
+def _import_reference():
+    """The installed reference package; its __init__ imports the missing
+    fastnmt.engine, so a stub is registered first."""
+    import types
+    if "fastnmt.engine" not in sys.modules:
+        stub = types.ModuleType("fastnmt.engine")
+        stub.RunConfig = type("RunConfig", (), {})
+        stub.Translator = type("Translator", (), {})
+        sys.modules["fastnmt.engine"] = stub
+    if str(REF_DIR) not in sys.path:
+        sys.path.insert(0, str(REF_DIR))
+    import fastnmt.model as M
+    import fastnmt.search as Sr
+    import fastnmt.store as St
+    return M, Sr, St
+
+
+def _cpu_init(impl, model_cfg, beam):
+    os.environ["OMP_NUM_THREADS"] = "1"
+    _CPU.update(impl=impl, beam=beam)
+    if impl == "reference":
+        M, Sr, St = _import_reference()
+        cfg = M.ModelConfig(**model_cfg)
+        _CPU["model"] = M.TranslationModel(cfg, St.random_model(cfg, 0))
+        _CPU["search"] = Sr
+    else:
+        from oracle import nmt_oracle as O
+        from paper_2109_08003_b200 import store as S
+        a = O.arch_of(S.ModelConfig(**model_cfg))
+        _CPU.update(arch=a, params=O.make_params(a, 0))
+
+
+def _cpu_ready(_):
+    return True
 
 
 def _cpu_worker(rows):
+    """One reference batch (the process's sentences, right-padded)."""
     from oracle import nmt_oracle as O
-    a, p, k = _CPU_STATE["arch"], _CPU_STATE["params"], _CPU_STATE["beam"]
     tok, valid = O.pad_rows(rows)
-    out = O.greedy(a, p, tok, valid) if k == 1 else O.beam(a, p, tok, valid, k)
-    return sum(len(o) for o in out), sum(len(r) for r in rows)
+    k = _CPU["beam"]
+    if _CPU["impl"] == "reference":
+        Sr, m = _CPU["search"], _CPU["model"]
+        sc = Sr.SearchConfig(bos_id=2, eos_id=3, pad_id=0, beam_size=k)
+        enc = m.encode(tok, valid)
+        out = Sr.greedy_translate(m, enc, sc) if k == 1 else Sr.beam_translate(m, enc, sc)
+    else:
+        a, p = _CPU["arch"], _CPU["params"]
+        out = O.greedy(a, p, tok, valid) if k == 1 else O.beam(a, p, tok, valid, k)
+    return [list(map(int, o)) for o in out]
 
 
-def cpu_run(rows_per_proc, procs):
-    """Translate procs x rows_per_proc sentences, one process per core (fork),
-    OMP_NUM_THREADS=1 (PAPER.md:179 'one MKL thread for each process')."""
-    import multiprocessing as mp
-    ctx = mp.get_context("fork")
-    t0 = time.perf_counter()
-    with ctx.Pool(procs) as pool:
-        res = pool.map(_cpu_worker, rows_per_proc)
-    dt = time.perf_counter() - t0
-    return sum(r[0] for r in res), sum(r[1] for r in res), dt
+class CpuArm:
+    def __init__(self, model_cfg, beam):
+        import multiprocessing as mp
+        from concurrent.futures import ProcessPoolExecutor
+        self.impl = "reference" if reference_available() else "port"
+        self.procs = os.cpu_count() or 1
+        # greedy: one 8-sentence reference batch per process per step; beam
+        # searches sentence by sentence anyway (search.py:105-111)
+        self.per_proc = PER_PROC if beam == 1 else 1
+        os.environ["OMP_NUM_THREADS"] = "1"   # inherited by the forkserver (numpy import)
+        self.pool = ProcessPoolExecutor(self.procs, mp_context=mp.get_context("forkserver"),
+                                        initializer=_cpu_init,
+                                        initargs=(self.impl, model_cfg, beam))
+        list(self.pool.map(_cpu_ready, range(4 * self.procs)))   # all initializers ran
+
+    def step(self, ids, offsets, start):
+        """procs x per_proc consecutive sentences from `start`, length-sorted and
+        dealt out in batches of per_proc (the reference planner's sort-then-group,
+        batching.py:100-109); returns (outputs in corpus order, src words, seconds)."""
+        n = self.procs * self.per_proc
+        order = sorted(range(start, start + n), key=lambda i: -(offsets[i + 1] - offsets[i]))
+        groups = [order[j * self.per_proc:(j + 1) * self.per_proc] for j in range(self.procs)]
+        jobs = [[ids[offsets[i]:offsets[i + 1]].astype(np.int64) for i in g] for g in groups]
+        t0 = time.perf_counter()
+        res = list(self.pool.map(_cpu_worker, jobs, chunksize=1))
+        dt = time.perf_counter() - t0
+        out = [None] * n
+        for g, r in zip(groups, res):
+            for i, o in zip(g, r):
+                out[i - start] = o
+        return out, sum(len(r) for j in jobs for r in j), dt
+
+    def run(self, ids, offsets, start, steps):
+        outs, src, total = [], 0, 0.0
+        for i in range(steps):
+            o, s, dt = self.step(ids, offsets, start + i * self.procs * self.per_proc)
+            outs += o
+            src += s
+            total += dt
+        return outs, src, total
+
+    def describe(self, steps, words, src, seconds, what):
+        kind = ("the unmodified reference package (baseline/_ref fastnmt, greedy_translate / "
+                "beam_translate)" if self.impl == "reference" else
+                "the oracle port (oracle/nmt_oracle.py, pinned bit-exact to the reference)")
+        return (f"{steps} steps x {self.procs} procs x {self.per_proc} length-sorted corpus "
+                f"sentences "
+                f"{what} ({words} target words, {src} source words, {seconds:.1f} s), {kind}, "
+                f"f32 numpy, one thread per process")
+
+    def close(self):
+        self.pool.shutdown(wait=True)
 
 
-def cpu_setup(model_cfg=None, beam=1):
-    """The selected model (BASELINE config of --model) with random_model(cfg, 0)
-    weights, greedy or beam as --beam says."""
-    os.environ["OMP_NUM_THREADS"] = "1"
+def parity_report(model_cfg, beam, dtype, sample_rows, got, want):
+    """GPU output vs the CPU arm's output on the same sentences (oracle/parity.py
+    bar; the oracle re-runs the divergent sentences for the near-tie report)."""
     from oracle import nmt_oracle as O
+    from oracle import parity as P
     from paper_2109_08003_b200 import store as S
-    a = O.arch_of(S.ModelConfig(**(model_cfg or CFG)))
-    _CPU_STATE["arch"] = a
-    _CPU_STATE["params"] = O.make_params(a, 0)
-    _CPU_STATE["beam"] = beam
+    tie = P.NEAR_TIE_BF16 if dtype == "bf16" else P.NEAR_TIE
+    a = O.arch_of(S.ModelConfig(**model_cfg))
+    bad = any(list(g) != list(w) for g, w in zip(got, want))
+    p = O.make_params(a, 0) if bad else None
+    rep = P.near_tie_report(a, p, sample_rows, got, want, beam, tie)
+    rep["divergences"] = rep["divergences"][:20]
+    return rep
 
 
-def cpu_sample(ids, offsets, start, procs, per_proc):
-    rows, k = [], start
-    for _ in range(procs):
-        grp = []
-        for _ in range(per_proc):
-            grp.append(ids[offsets[k]:offsets[k + 1]].astype(np.int64))
-            k += 1
-        rows.append(grp)
-    return rows, k
+FIXTURES = {("6-1-1", 1): ("s611", 65536), ("6-1-8", 1): ("s618", 65536),
+            ("6-6-8", 4): ("s668_beam4", 8192), ("deep-12-768", 4): ("deep_beam4", 8192)}
 
 
-def cpu_baseline(ids, offsets, seconds, model_cfg=None, beam=1):
-    cpu_setup(model_cfg, beam)
-    procs = os.cpu_count() or 1
-    # calibrate per-process sample size to ~`seconds` of work (~55 words/s/core for
-    # Student-6-1-1 greedy, SURVEY §6; the beam / larger configs run ~15-20x slower)
-    rate = 55.0 if (beam == 1 and (model_cfg or CFG)["n_dec_layers"] == 1) else 3.0
-    per_proc = max(1, int(seconds * rate / 41.25 / 1.5))
-    rows, _ = cpu_sample(ids, offsets, 0, procs, per_proc)
-    words, src, dt = cpu_run(rows, procs)
-    return {"value": words / dt, "unit": UNIT, "cores": procs, "kind": "port",
-            "sample": f"{procs} procs x {per_proc} sentences of the synthetic corpus "
-                      f"({words} target words, {src} source words, {dt:.1f} s), oracle/nmt_oracle.py "
-                      f"f32 numpy {'greedy' if beam == 1 else f'beam {beam}'}, one thread per process"}
+def fixture_parity(eng, args, cfg, ids, offsets, lengths):
+    """The engine (same caps, default lanes) on corpus chunk 0 vs the committed
+    reference outputs for its sampled sentences (tests/golden/corpus_*.npz,
+    oracle/make_golden_corpus.py); untimed."""
+    from oracle import parity as P
+    key = FIXTURES.get((args.model, args.beam))
+    path = ROOT / "tests" / "golden" / f"corpus_{key[0]}.npz" if key else None
+    if not path or not path.exists() or args.dtype not in ("f16", "bf16"):
+        return None
+    from paper_2109_08003_b200.engine import budgets_of
+    fx = np.load(path)
+    n = min(key[1], len(lengths))
+    out, olen, oof, _ = eng.translate(ids, offsets[:n + 1], sbatch=SBATCH, wbatch=WBATCH,
+                                      beam=args.beam)
+    got = [out[oof[i]:oof[i] + olen[i]].tolist() for i in fx["idx"]]
+    tie = P.NEAR_TIE_BF16 if args.dtype == "bf16" else P.NEAR_TIE
+    if args.beam == 1:
+        rep = P.greedy_report(got, fx, near_tie=tie)
+    else:
+        rep = P.beam_report(got, fx, budgets_of(lengths[fx["idx"]], 1.5, 5, cfg.max_positions),
+                            near_tie=tie)
+    rep["divergences"] = rep["divergences"][:20]
+    return {"workload": f"corpus chunk 0 (first {n} sentences, caps {SBATCH}/{WBATCH}, default "
+                        f"lanes) vs the reference's recorded outputs for {len(fx['idx'])} of them "
+                        f"({path.name})", **rep}
 
 
 def arm_config(args, world):
@@ -248,40 +354,32 @@ def arm_config(args, world):
 
 
 def run_reference(args):
-    """--impl reference: the reference algorithm's CPU path (oracle port of
-    fastnmt, /root/reference is not on the GPU box) on all host cores."""
+    """--impl reference: the reference's own CPU path on all host cores —
+    the unmodified fastnmt package from baseline/_ref (plain pip install of
+    /root/reference/pkg; no engine, kernels or code of ours on that path),
+    or the oracle port when that install is absent.  Each step translates a
+    bounded sample (procs x PER_PROC consecutive corpus sentences)."""
     world, rank, _ = dist_env()
     if rank != 0:
         return 0
     from paper_2109_08003_b200.synthetic import newstest_corpus
     model_cfg = MODELS[args.model][1]
     ids, offsets, _ = newstest_corpus(CORPUS, model_cfg["vocab_size"])
-    cpu_setup(model_cfg, args.beam)
-    procs = os.cpu_count() or 1
-    per_proc = 2 if args.beam == 1 and model_cfg["n_dec_layers"] == 1 else 1
-    k = 0
-    for _ in range(args.warmup):
-        rows, k = cpu_sample(ids, offsets, k, procs, 1)
-        cpu_run(rows, procs)
-    words = src = 0
-    total = 0.0
-    for _ in range(args.steps):
-        rows, k = cpu_sample(ids, offsets, k, procs, per_proc)
-        w, s, dt = cpu_run(rows, procs)
-        words += w
-        src += s
-        total += dt
+    arm = CpuArm(model_cfg, args.beam)
+    per_step = arm.procs * arm.per_proc
+    arm.run(ids, offsets, 0, args.warmup)
+    outs, src, total = arm.run(ids, offsets, args.warmup * per_step, args.steps)
+    arm.close()
+    words = sum(len(o) for o in outs)
     value = words / total
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic", "impl": "reference",
             "config": arm_config(args, 1),
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": "port",
-                             "sample": f"{args.steps} steps x {procs} procs x {per_proc} sentences "
-                                       f"of the same corpus ({words} target words), the "
-                                       f"reference algorithm (oracle/nmt_oracle.py, f32 numpy, "
-                                       f"pinned to the reference) on the host cores"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": arm.procs, "kind": arm.impl,
+                             "sample": arm.describe(args.steps, words, src, total,
+                                                    "(after the warm-up steps' sentences)")},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
@@ -487,9 +585,35 @@ def main():
         # whole-step algorithmic rate (63.8 MFLOP / target word)
         roofline["step_tflops"] = round(sum(p["flops"] for p in prof.values()) / (total_ms * 1e9), 2)
 
-    cpu = None
+    # ---- CPU baseline + parity on the timed workload -------------------------
+    # The CPU arm translates the first sentences of the LAST timed e2e step's
+    # chunk; the GPU's output for them is what that step left in pin_out.
+    cpu = parity = None
     if world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(ids, offsets, args.cpu_seconds, model_cfg, BEAM)
+        arm = CpuArm(model_cfg, BEAM)
+        c_last = chunk_of(W + K - 1)
+        lo, hi, L, b, off = chunk_meta[c_last]
+        steps = max(1, int(round(args.cpu_seconds / (6.0 if BEAM == 1 else 12.0))))
+        want, src, dt = arm.run(ids, offsets, lo, steps)
+        arm.close()
+        n = len(want)
+        got = [pin_out[int(off[i]):int(off[i]) + int(pin_len[i])].tolist() for i in range(n)]
+        words = sum(len(o) for o in want)
+        cpu = {"value": words / dt, "unit": UNIT, "cores": arm.procs, "kind": arm.impl,
+               "sample": arm.describe(steps, words, src, dt, f"from chunk {c_last}")}
+        sample_rows = [ids[offsets[i]:offsets[i + 1]].astype(np.int64) for i in range(lo, lo + n)]
+        live = {"workload": f"the last timed e2e step (chunk {c_last}, caps {SBATCH}/{WBATCH}, "
+                            f"default lanes) vs the CPU arm on its first {n} sentences",
+                **parity_report(model_cfg, BEAM, args.dtype, sample_rows, got, want)}
+        fixed = fixture_parity(eng, args, cfg, ids, offsets, lengths)
+        parts = [x for x in (live, fixed) if x]
+        tot = sum(x["sentences"] for x in parts)
+        same = sum(x["identical"] for x in parts)
+        parity = {"sentences": tot, "identical": same, "identical_frac": same / max(tot, 1),
+                  "all_near_ties": all(x["all_near_ties"] for x in parts),
+                  "pass": all(x["pass"] for x in parts) and
+                          same >= live["min_identical_frac"] * tot,
+                  "live": live, "fixture": fixed}
 
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
@@ -501,6 +625,7 @@ def main():
         "gpu_launches": int(launches),
         "roofline": roofline,
         "cpu_baseline": cpu,
+        "parity": parity,
         "clocks": clocks,
         "peak_hbm_gb": round(max(peak_alloc, engine_bytes + peak_alloc) / 1e9, 3),
         "engine_device_gb": round(engine_bytes / 1e9, 3),

@@ -53,7 +53,7 @@ typedef struct fnmt_arch {
  * (search.py:28-39). */
 typedef struct fnmt_run {
   int32_t sbatch, wbatch;     /* DecodeLimits (batching.py:35-42) */
-  float max_len_ratio;        /* 1.5 */
+  double max_len_ratio;       /* 1.5; binary64 like the reference's Python float */
   int32_t max_len_offset;     /* 5 */
   int32_t beam_size;          /* 1 = greedy */
   int32_t bos_id, eos_id, pad_id;
@@ -163,7 +163,7 @@ int fnmt_engine_reserve(fnmt_engine* e, const fnmt_run* run);
 
 /* Output budget per sentence: max(1, min(maxpos, ceil(ratio*len)+offset))
  * (search.py:49-51); writes budgets[n] and returns their sum (or <0). */
-int64_t fnmt_budgets(const int32_t* lengths, int n, float ratio, int offset, int max_positions,
+int64_t fnmt_budgets(const int32_t* lengths, int n, double ratio, int offset, int max_positions,
                      int32_t* budgets);
 
 /* Corpus-level greedy translation (greedy_translate over plan_batches,

@@ -343,8 +343,24 @@ def out_budget(src_len: int, max_positions: int, ratio: float = 1.5, offset: int
     return max(1, min(max_positions, math.ceil(ratio * src_len) + offset))
 
 
-def greedy(a: Arch, p: dict, tokens, valid, ratio=1.5, offset=5, bos=BOS, eos=EOS, pad=PAD):
-    """search.py:58-86.  Returns list of id lists (no BOS/EOS)."""
+def top2_of(logits):
+    """Per row: (top-1 value, top-2 value, top-2 id); top-1 is np.argmax's
+    lowest-id maximum (search.py:71), top-2 the best of the rest."""
+    rows = np.arange(logits.shape[0])
+    i1 = np.argmax(logits, axis=1)
+    v1 = logits[rows, i1].copy()
+    rest = logits.copy()
+    rest[rows, i1] = -np.inf
+    i2 = np.argmax(rest, axis=1)
+    return v1, rest[rows, i2].copy(), i2.astype(np.int32)
+
+
+def greedy(a: Arch, p: dict, tokens, valid, ratio=1.5, offset=5, bos=BOS, eos=EOS, pad=PAD,
+           trace=None):
+    """search.py:58-86.  Returns list of id lists (no BOS/EOS).
+
+    ``trace`` (a list) receives one ``top2_of`` triple per step (all rows), the
+    near-tie evidence for the fp16/bf16 parity reports."""
     valid = np.asarray(valid, bool)
     n = valid.shape[0]
     if n == 0:
@@ -356,7 +372,10 @@ def greedy(a: Arch, p: dict, tokens, valid, ratio=1.5, offset=5, bos=BOS, eos=EO
     done = np.zeros(n, bool)
     res = [[] for _ in range(n)]
     for t in range(max(budget)):
-        best = np.argmax(decoder_step(a, p, c, feed), axis=1)
+        logits = decoder_step(a, p, c, feed)
+        best = np.argmax(logits, axis=1)
+        if trace is not None:
+            trace.append(top2_of(logits))
         feed = np.full(n, pad, np.int64)
         for r in np.flatnonzero(~done):
             tok = int(best[r])
@@ -378,12 +397,17 @@ def log_softmax64(logits):
 
 
 def beam_sentence(a: Arch, p: dict, states_row, valid_row, k: int,
-                  ratio=1.5, offset=5, bos=BOS, eos=EOS):
+                  ratio=1.5, offset=5, bos=BOS, eos=EOS, trace=None, trace_width=None):
     """search.py:114-147 for one sentence (states_row [1,s,d]).
 
     Candidate order is (score desc, token asc, parent asc); an EOS pick moves
     the hypothesis to the finished pool and still consumes one of the k slots.
     Returns (tokens, score, finished).
+
+    ``trace`` (a list) receives, per step, the first ``trace_width`` (default
+    3k) candidates in that order as (score f64, token, parent) arrays: enough
+    to replay the search and to measure how close any other hypothesis came
+    to being kept (the near-tie report of the GPU beam parity tests).
     """
     limit = out_budget(int(np.asarray(valid_row).sum()), a.max_positions, ratio, offset)
     c = start_cache(a, p, states_row, valid_row)
@@ -399,7 +423,13 @@ def beam_sentence(a: Arch, p: dict, states_row, valid_row, k: int,
         tok = np.tile(np.arange(lp.shape[1]), len(live))
         flat = sc.reshape(-1)
         # python float addition == numpy float64 addition (both IEEE binary64)
-        order = np.lexsort((par, tok, -flat))[:k]
+        if trace is not None:
+            wide = np.lexsort((par, tok, -flat))[:trace_width or 3 * k]
+            trace.append((flat[wide].astype(np.float64), tok[wide].astype(np.int32),
+                          par[wide].astype(np.int32)))
+            order = wide[:k]
+        else:
+            order = np.lexsort((par, tok, -flat))[:k]
         nxt, parents = [], []
         for j in order:
             sj, tj, pj = float(flat[j]), int(tok[j]), int(par[j])
@@ -418,6 +448,71 @@ def beam_sentence(a: Arch, p: dict, states_row, valid_row, k: int,
         pool, finished = live, False
     best = max(pool, key=lambda h: (h[1], tuple(-x for x in h[0])))
     return list(best[0]), best[1], finished
+
+
+def beam_divergence(steps, k: int, hyp, budget: int, eos=EOS):
+    """Near-tie measure for a beam output ``hyp`` that differs from the
+    oracle's.  ``steps`` is a ``beam_sentence`` trace (per step: candidate
+    scores / tokens / parents in the reference's sort order, search.py:125-127).
+
+    Replays the oracle search along ``hyp``'s path and returns
+    (where, step, gap):
+      * ("step", t, gap): at step t the oracle did not keep hyp's prefix
+        extension; gap = score of the oracle's k-th kept candidate minus the
+        score of hyp's candidate (inf when it is outside the traced width);
+      * ("final", t, gap): hyp survived every step; gap = oracle best final
+        score minus hyp's final score (search.py:145-147).
+    ``hyp`` finished with EOS iff len(hyp) < budget (search.py:116-140).
+    """
+    hyp = tuple(int(x) for x in hyp)
+    finished = len(hyp) < budget
+    live, fin = [((), 0.0)], []
+    t = -1
+    for t, (sc, tok, par) in enumerate(steps):
+        want = hyp[t] if t < len(hyp) else eos
+        if t >= len(hyp) and not finished:
+            break
+        prefix = hyp[:t]
+        pidx = next((i for i, h in enumerate(live) if h[0] == prefix), None)
+        if pidx is None:
+            return ("step", t, float("inf"))
+        hit = [j for j in range(len(tok)) if int(tok[j]) == want and int(par[j]) == pidx]
+        if not hit or hit[0] >= k:
+            gap = float(sc[k - 1] - sc[hit[0]]) if hit else float("inf")
+            return ("step", t, gap)
+        nxt = []
+        for j in range(min(k, len(tok))):
+            pj, tj, sj = int(par[j]), int(tok[j]), float(sc[j])
+            if tj == eos:
+                fin.append((live[pj][0], sj))
+            else:
+                nxt.append((live[pj][0] + (tj,), sj))
+        live = nxt
+        if want == eos or not live or len(fin) >= k:
+            break
+    pool = fin if fin else live
+    best = max(pool, key=lambda h: (h[1], tuple(-x for x in h[0])))
+    mine = [h for h in pool if h[0] == hyp]
+    if not mine:
+        return ("final", t, float("inf"))
+    return ("final", t, float(best[1] - mine[0][1]))
+
+
+def greedy_divergence(ref, got, top1, top2, top2_id):
+    """First divergent step of a greedy output and the reference's top-1 minus
+    top-2 logit gap there (inf if ``got`` took a token other than the
+    reference's runner-up).  top*/top2_id are the reference's per-step values
+    for this sentence.  Returns None when the outputs are identical."""
+    ref, got = list(ref), list(got)
+    if ref == got:
+        return None
+    j = next((i for i in range(min(len(ref), len(got))) if ref[i] != got[i]),
+             min(len(ref), len(got)))
+    if j >= len(top1):
+        return (j, float("inf"))
+    alt = got[j] if j < len(got) else EOS
+    gap = float(top1[j] - top2[j]) if int(top2_id[j]) == alt else float("inf")
+    return (j, gap)
 
 
 def beam(a: Arch, p: dict, tokens, valid, k: int, ratio=1.5, offset=5):

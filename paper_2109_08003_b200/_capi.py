@@ -25,7 +25,7 @@ class fnmt_arch(C.Structure):
 
 
 class fnmt_run(C.Structure):
-    _fields_ = [("sbatch", C.c_int32), ("wbatch", C.c_int32), ("max_len_ratio", C.c_float),
+    _fields_ = [("sbatch", C.c_int32), ("wbatch", C.c_int32), ("max_len_ratio", C.c_double),
                 ("max_len_offset", C.c_int32), ("beam_size", C.c_int32), ("bos_id", C.c_int32),
                 ("eos_id", C.c_int32), ("pad_id", C.c_int32)]
 
@@ -71,7 +71,7 @@ _SIGNATURES = {
     "fnmt_engine_set_qtensor": (_I, [_VP, C.c_char_p, _VP, _VP, _VP, _I64, _I64]),
     "fnmt_engine_finalize": (_I, [_VP]),
     "fnmt_engine_reserve": (_I, [_VP, C.POINTER(fnmt_run)]),
-    "fnmt_budgets": (_I64, [_VP, _I, _F, _I, _I, _VP]),
+    "fnmt_budgets": (_I64, [_VP, _I, C.c_double, _I, _I, _VP]),
     "fnmt_engine_translate": (_I, [_VP, _VP, _VP, _I, C.POINTER(fnmt_run), _VP, _VP, _VP,
                                    C.POINTER(fnmt_stats)]),
     "fnmt_engine_translate_device": (_I, [_VP, _VP, _VP, _VP, _I, C.POINTER(fnmt_run), _VP, _VP,

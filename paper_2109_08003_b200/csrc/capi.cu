@@ -332,7 +332,7 @@ int fnmt_engine_reserve(fnmt_engine* e, const fnmt_run* run) {
   });
 }
 
-int64_t fnmt_budgets(const int32_t* lengths, int n, float ratio, int offset, int max_positions,
+int64_t fnmt_budgets(const int32_t* lengths, int n, double ratio, int offset, int max_positions,
                      int32_t* budgets) {
   if ((!lengths && n) || n < 0 || max_positions < 1) {
     fnmt::set_error("fnmt_budgets: bad arguments");

@@ -165,9 +165,10 @@ std::vector<Batch> plan_batches(const std::vector<int32_t>& lengths, int sbatch,
   return out;
 }
 
-int budget_of(int32_t len, float ratio, int offset, int max_positions) {
-  // search.py:49-51 (python float math: ceil(ratio * len) in double)
-  const double v = std::ceil((double)ratio * (double)len) + offset;
+int budget_of(int32_t len, double ratio, int offset, int max_positions) {
+  // search.py:49-51 (python float math: ceil(ratio * len) in binary64; the ratio
+  // crosses the C ABI as a double so e.g. 1.2 is the same value Python multiplies)
+  const double v = std::ceil(ratio * (double)len) + offset;
   int64_t b = (int64_t)v;
   b = std::min<int64_t>(b, max_positions);
   return (int)std::max<int64_t>(1, b);

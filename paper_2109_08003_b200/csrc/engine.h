@@ -65,7 +65,7 @@ struct Batch {
   bool oversize = false;
 };
 std::vector<Batch> plan_batches(const std::vector<int32_t>& lengths, int sbatch, int wbatch);
-int budget_of(int32_t len, float ratio, int offset, int max_positions);
+int budget_of(int32_t len, double ratio, int offset, int max_positions);
 
 struct Workspace {
   int tok_cap = 0, row_cap = 0;

@@ -76,15 +76,23 @@ class Engine:
             offsets, np.ndarray) else offsets
         n = len(offsets) - 1
         lengths = np.diff(np.asarray(offsets)).astype(np.int32)
+        b, planned_off = self.plan_outputs(lengths, ratio, offset)
         if out_off is None:
-            b, out_off = self.plan_outputs(lengths, ratio, offset)
-            total = int(b.sum())
+            out_off = planned_off
         else:
-            total = None
+            out_off = np.ascontiguousarray(out_off, dtype=np.int64)
+            if out_off.shape != (n,) or (n and out_off.min() < 0):
+                raise ValueError(f"out_off must be {n} non-negative int64 offsets")
+        # the native call writes sentence i's ids at out_ids[out_off[i] : +budget_i]
+        total = int((out_off + b).max()) if n else 0
         if out_ids is None:
-            out_ids = np.empty(max(total or 0, 1), dtype=np.int32)
+            out_ids = np.empty(max(total, 1), dtype=np.int32)
+        elif len(out_ids) < total:
+            raise ValueError(f"out_ids holds {len(out_ids)} ids, the budgets need {total}")
         if out_len is None:
             out_len = np.empty(max(n, 1), dtype=np.int32)
+        elif len(out_len) < n:
+            raise ValueError(f"out_len holds {len(out_len)} entries, need {n}")
         st = _capi.fnmt_stats()
         r = run_struct(sbatch, wbatch, ratio, offset, beam)
         check(lib.fnmt_engine_translate(self.handle.h, ptr(ids), ptr(offsets), n, C.byref(r),

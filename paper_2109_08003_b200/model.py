@@ -33,6 +33,9 @@ _TORCH_DT = {_capi.F32: torch.float32, _capi.F16: torch.float16, _capi.BF16: tor
              _capi.INT8: torch.float32}   # int8 engines keep f32 activations
 
 
+MAX_DEVICE_BEAM = 8   # fused top-K epilogue width (csrc kTopKMax)
+
+
 class LengthError(ValueError):
     """Input exceeds the model's position budget (model.py:41-42)."""
 
@@ -212,6 +215,14 @@ class GpuTranslationModel:
         tokens = self._check_tokens(tokens)
         pad_mask = np.asarray(pad_mask, dtype=bool)
         b, s = tokens.shape
+        if pad_mask.shape != (b, s):
+            raise ValueError(f"pad_mask shape {pad_mask.shape} != tokens shape {(b, s)}")
+        lens = pad_mask.sum(axis=1)
+        if not np.array_equal(pad_mask, np.arange(s)[None, :] < lens[:, None]):
+            # the packed-varlen encoder reads row r's keys as its first len_r
+            # positions; a left-padded or gapped mask would be silently wrong
+            raise ValueError("the GPU engine expects right-padded sources (pad_mask must be "
+                             "True on a prefix of each row)")
         if s > self.cfg.max_positions:
             raise LengthError(f"source length {s} exceeds max_positions {self.cfg.max_positions}")
         d = self.cfg.d_model
@@ -276,11 +287,12 @@ class GpuTranslationModel:
     def beam_batch(self, enc: GpuEncoderOutput, cfg) -> list[list[int]]:
         """Beam search (search.py:105-147).  Batched on the device: fused
         vocab top-K epilogue, per-sentence selection kernel, ancestor-table
-        KV reuse.  Rows whose source is entirely masked keep the reference's
-        all-masked attention semantics through the protocol loop."""
+        KV reuse (beam sizes up to MAX_DEVICE_BEAM).  Larger beams, and rows
+        whose source is entirely masked (the reference's all-masked attention
+        semantics), run the reference's per-sentence search over step()."""
         from .search import _beam_sentence, _device_rows
         rows = _device_rows(self, enc)
-        if rows is not None:
+        if rows is not None and cfg.beam_size <= MAX_DEVICE_BEAM:
             return self.translate_batch(rows, search=cfg)
         lens = enc.pad_mask.sum(axis=1)
         return [_beam_sentence(self, self.init_cache(enc.row(r)), int(lens[r]), cfg)

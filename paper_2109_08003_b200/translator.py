@@ -73,16 +73,29 @@ class RunConfig:
         for name in ("sbatch", "wbatch", "workers", "chunk_lines", "beam"):
             if getattr(self, name) < 1:
                 raise ValueError(f"{name} must be >= 1")
+        if self.beam > 8:
+            # the engine's corpus path keeps beam state in the fused top-K vocab
+            # epilogue (up to 8 candidates per row); GpuTranslationModel's
+            # protocol-level beam_translate has no cap
+            raise ValueError(f"beam={self.beam}: the GPU Translator supports beam sizes 1-8")
         if not self.devices or any(int(d) < 0 for d in self.devices):
             raise ValueError("devices must list at least one CUDA ordinal")
         object.__setattr__(self, "devices", tuple(int(d) for d in self.devices))
 
 
-# Text stages in forked worker processes (run.workers > 1): pure-Python
-# tokenize / BPE / detokenize are GIL-bound, so threads do not scale; the
-# workers inherit the Translator (vocabulary, codec, word caches) at fork time
-# and never touch CUDA.
-_FORK_TEXT = None
+# Text stages in worker processes (run.workers > 1): pure-Python tokenize /
+# BPE / detokenize are GIL-bound, so threads do not scale.  The workers come
+# from a "forkserver" context — a clean server process that never touched
+# CUDA or the engine's lane threads (forking the multi-threaded,
+# CUDA-initialised translator process itself is unsafe) — and receive a
+# pickled copy of the text stage (vocabulary, codec, split limit) once, in
+# their initializer.
+_WORKER_STAGE = None
+
+
+def _init_worker(stage):
+    global _WORKER_STAGE
+    _WORKER_STAGE = stage
 
 
 def _proc_ready(_):
@@ -90,11 +103,11 @@ def _proc_ready(_):
 
 
 def _proc_to_ids(lines, pretok):
-    return _FORK_TEXT._to_ids(lines, pretok)
+    return _WORKER_STAGE.to_ids(lines, pretok)
 
 
 def _proc_to_text(chunk, outs, pretok):
-    return _FORK_TEXT._to_text(chunk, outs, pretok)
+    return _WORKER_STAGE.to_text(chunk, outs, pretok)
 
 
 @dataclass
@@ -102,6 +115,90 @@ class _Chunk:
     pieces: list          # list[np.ndarray int32] subword ids, each <= limit
     owner: list           # piece -> line index within the chunk
     n_lines: int
+
+
+class _TextStage:
+    """Host text stages of one (vocabulary, codec, split limit): word-memoised
+    tokenize -> BPE -> ids and ids -> BPE-join -> detokenize, plus the worker
+    pools that run them.  ``Translator.with_run`` copies share their stage
+    (same codec, same pools); assigning ``Translator.codec`` gives that
+    translator a fresh stage and leaves the others' pools alone.  Pools close
+    when the last translator holding the stage goes away."""
+
+    def __init__(self, vocab: Vocabulary, codec: Optional[BpeCodec], limit: int):
+        self.vocab = vocab
+        self.codec = codec
+        self.limit = limit
+        self.word_ids = {False: {}, True: {}}   # per pretokenized flag: word -> ids
+        self.pools: dict = {}                   # workers -> process pool
+
+    def __getstate__(self):   # what a worker receives: no pools, empty caches
+        return {"vocab": self.vocab, "codec": self.codec, "limit": self.limit}
+
+    def __setstate__(self, st):
+        self.__dict__.update(st)
+        self.word_ids = {False: {}, True: {}}
+        self.pools = {}
+
+    def pool(self, n: int):
+        """The text-stage process pool for n workers (started eagerly, once)."""
+        pool = self.pools.get(n)
+        if pool is None:
+            pool = ProcessPoolExecutor(max_workers=n, mp_context=mp.get_context("forkserver"),
+                                       initializer=_init_worker, initargs=(self,))
+            list(pool.map(_proc_ready, range(n)))
+            self.pools[n] = pool
+        return pool
+
+    def close(self) -> None:
+        for pool in self.pools.values():
+            pool.shutdown(wait=False, cancel_futures=True)
+        self.pools.clear()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:   # noqa: BLE001 - interpreter teardown
+            pass
+
+    def word(self, word: str, pretok: bool) -> tuple:
+        toks = [word] if pretok else tokenize_word(word)
+        if self.codec is not None:
+            toks = bpe_encode(toks, self.codec)
+        return tuple(self.vocab.encode(toks))
+
+    def to_ids(self, lines: Sequence[str], pretok: bool) -> "_Chunk":
+        """tokenize -> BPE -> vocab ids.  All three stages act word by word
+        (textpipe.tokenize splits the cleaned line on whitespace first), so the
+        ids of each distinct word are memoised: a Zipfian corpus turns into
+        dict lookups after its first few thousand lines."""
+        pieces, owner = [], []
+        cache = self.word_ids[pretok]
+        for li, line in enumerate(lines):
+            ids: list = []
+            for w in (line.split() if pretok else clean_line(line).split()):
+                t = cache.get(w)
+                if t is None:
+                    t = self.word(w, pretok)
+                    if len(cache) < _WORD_CACHE_MAX:
+                        cache[w] = t
+                ids.extend(t)
+            arr = np.asarray(ids, dtype=np.int32)
+            for s in range(0, len(arr), self.limit):
+                pieces.append(arr[s:s + self.limit])
+                owner.append(li)
+        return _Chunk(pieces, owner, len(lines))
+
+    def to_text(self, chunk: "_Chunk", outs: list, pretok: bool) -> list:
+        per_line = [[] for _ in range(chunk.n_lines)]
+        tok = self.vocab.token_of
+        for li, ids in zip(chunk.owner, outs):
+            per_line[li].extend(tok(int(i)) for i in ids)
+        res = []
+        for sub in per_line:
+            words = bpe_decode(sub) if self.codec is not None else sub
+            res.append(" ".join(words) if pretok else detokenize(words))
+        return res
 
 
 class Translator:
@@ -113,16 +210,14 @@ class Translator:
             raise ValueError(f"vocabulary has {len(vocab)} entries, config says "
                              f"{self.cfg.vocab_size}")
         self.vocab = vocab
-        self._word_ids = {False: {}, True: {}}   # per pretokenized flag: word -> ids
-        self._pools: dict = {}                   # workers -> forked text-stage pool
-        self.codec = codec
+        self.limit = max(1, min(HARD_SPLIT, self.cfg.max_positions))
+        self._text = _TextStage(vocab, codec, self.limit)
         self.run = run
         self.weights = weights
         devs = run.devices if run.devices != (0,) else (device,)
         # one engine (weights + workspace + CUDA graphs) per listed device
         self.engines = [Engine(self.cfg, weights, dtype=run.precision, device=d) for d in devs]
         self.engine = self.engines[0]
-        self.limit = max(1, min(HARD_SPLIT, self.cfg.max_positions))
 
     @classmethod
     def from_file(cls, path, run: RunConfig = RunConfig(), bpe_codes=None,
@@ -144,80 +239,26 @@ class Translator:
 
     @property
     def codec(self) -> Optional[BpeCodec]:
-        return self._codec
+        return self._text.codec
 
     @codec.setter
     def codec(self, value: Optional[BpeCodec]) -> None:   # assignable, like the reference's
-        self._codec = value
-        self._word_ids = {False: {}, True: {}}
-        self.close_pools()   # forked workers hold the old codec
+        # a fresh stage (caches, pools) for this translator only: with_run copies
+        # keep the old codec and its workers
+        self._text = _TextStage(self.vocab, value, self.limit)
 
     def close_pools(self) -> None:
-        for pool in getattr(self, "_pools", {}).values():
-            pool.shutdown(wait=False, cancel_futures=True)
-        if hasattr(self, "_pools"):
-            self._pools.clear()
-
-    def __del__(self):
-        try:
-            self.close_pools()
-        except Exception:   # noqa: BLE001 - interpreter teardown
-            pass
-
-    def _proc_pool(self):
-        """The forked text-stage pool for run.workers (created once, workers
-        started eagerly so the fork happens here, outside any engine call)."""
-        global _FORK_TEXT
-        n = self.run.workers
-        pool = self._pools.get(n)
-        if pool is None:
-            _FORK_TEXT = self
-            pool = ProcessPoolExecutor(max_workers=n, mp_context=mp.get_context("fork"))
-            list(pool.map(_proc_ready, range(n)))
-            self._pools[n] = pool
-        return pool
+        """Shut down this translator's text-stage workers (recreated on demand)."""
+        self._text.close()
 
     # ---- host stages -------------------------------------------------------
-    def _word(self, word: str, pretok: bool) -> tuple:
-        toks = [word] if pretok else tokenize_word(word)
-        if self._codec is not None:
-            toks = bpe_encode(toks, self._codec)
-        return tuple(self.vocab.encode(toks))
-
     def _to_ids(self, lines: Sequence[str], pretok: Optional[bool] = None) -> _Chunk:
-        """tokenize -> BPE -> vocab ids.  All three stages act word by word
-        (textpipe.tokenize splits the cleaned line on whitespace first), so the
-        ids of each distinct word are memoised: a Zipfian corpus turns into
-        dict lookups after its first few thousand lines."""
-        pieces, owner = [], []
         pretok = self.run.pretokenized if pretok is None else pretok
-        cache = self._word_ids[pretok]
-        for li, line in enumerate(lines):
-            ids: list = []
-            for w in (line.split() if pretok else clean_line(line).split()):
-                t = cache.get(w)
-                if t is None:
-                    t = self._word(w, pretok)
-                    if len(cache) < _WORD_CACHE_MAX:
-                        cache[w] = t
-                ids.extend(t)
-            arr = np.asarray(ids, dtype=np.int32)
-            for s in range(0, len(arr), self.limit):
-                pieces.append(arr[s:s + self.limit])
-                owner.append(li)
-        return _Chunk(pieces, owner, len(lines))
+        return self._text.to_ids(lines, pretok)
 
     def _to_text(self, chunk: _Chunk, outs: list, pretok: Optional[bool] = None) -> list:
         pretok = self.run.pretokenized if pretok is None else pretok
-        per_line = [[] for _ in range(chunk.n_lines)]
-        tok = self.vocab.token_of
-        for li, ids in zip(chunk.owner, outs):
-            per_line[li].extend(tok(int(i)) for i in ids)
-        res = []
-        for sub in per_line:
-            words = bpe_decode(sub) if self._codec is not None else sub
-            res.append(" ".join(words) if pretok else detokenize(words))
-        return res
+        return self._text.to_text(chunk, outs, pretok)
 
     # ---- GPU stage -----------------------------------------------------------
     def _translate_pieces(self, pieces: list, engine=None) -> list:
@@ -259,7 +300,7 @@ class Translator:
         pretok = self.run.pretokenized
         procs = self.run.workers > 1
         with ThreadPoolExecutor(max_workers=1 if procs else self.run.workers) as tpool:
-            pool = self._proc_pool() if procs else tpool
+            pool = self._text.pool(self.run.workers) if procs else tpool
             pre_fn = _proc_to_ids if procs else self._to_ids
             post_fn = _proc_to_text if procs else self._to_text
 

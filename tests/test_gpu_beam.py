@@ -15,6 +15,7 @@ if not torch.cuda.is_available():
     pytest.skip("needs a CUDA device", allow_module_level=True)
 
 from oracle import nmt_oracle as O  # noqa: E402
+from oracle import parity as P  # noqa: E402
 from paper_2109_08003_b200 import store as S  # noqa: E402
 from paper_2109_08003_b200.engine import Engine  # noqa: E402
 from paper_2109_08003_b200.model import GpuTranslationModel  # noqa: E402
@@ -52,7 +53,12 @@ def test_student_beam_vs_reference(golden, tag, dtype):
         if dtype == "f32":
             assert got == want, (k, same)
         else:
-            assert same >= len(rows) - 1, (k, same)
+            # every fp16 divergence a near-tie of the oracle's beam scores
+            if same < len(rows):
+                a = O.arch_of(cfg)
+                rep = P.near_tie_report(a, O.make_params(a, 0), rows, got, want, beam=k)
+                print(tag, k, rep)
+                assert rep["all_near_ties"], rep
 
 
 def eos_biased(cfg, seed, bias):
@@ -82,7 +88,8 @@ def test_beam_with_eos_matches_oracle(k, bias):
     assert got_small == want
     eng16 = Engine(cfg, w, dtype="f16")
     got16 = run_engine(eng16, rows, k)
-    assert sum(x == y for x, y in zip(got16, want)) >= len(rows) - 2
+    rep = P.near_tie_report(a, p, rows, got16, want, beam=k)
+    assert rep["all_near_ties"], rep
 
 
 def test_beam1_equals_greedy_native(golden):

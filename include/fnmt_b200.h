@@ -81,9 +81,8 @@ int fnmt_linear(const void* A, int lda, int a_dtype, const void* W, int ldw, con
 /* x = norm(x + A . W^T + bias) * gain + beta in place (f32 x [M, N]), plus
  * its copy in the A dtype (x_act, may be NULL) — Projection.apply followed by
  * the post-norm residual block of encode / decode_step (model.py:279-286,
- * :327-343, tensor.py:98-129).  f16 / bf16 with N in {256, 512, 768, 1024}
- * run one clustered tcgen05 GEMM whose epilogue all-reduces the row
- * statistics through distributed shared memory; otherwise GEMM + add_norm. */
+ * :327-343, tensor.py:98-129): the GEMM adds into x in its epilogue, then one
+ * row kernel normalises. */
 int fnmt_linear_add_norm(const void* A, int lda, int a_dtype, const void* W, int ldw,
                          const float* bias, float* x, void* x_act, const float* gain,
                          const float* beta, int l1, int M, int N, int K, void* stream);

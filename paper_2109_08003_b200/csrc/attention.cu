@@ -253,23 +253,6 @@ __device__ __forceinline__ int64_t decode_key_row(const DecAttnArgs& a, const De
   return c.seq_row0 + j;
 }
 
-// Deterministic block-wide double sum (warp shuffles, then warp 0 over the
-// per-warp partials in order); `scratch` needs NT / 32 doubles and may alias
-// data no thread reads any more.
-template <int NT>
-__device__ __forceinline__ double block_sum_d(double v, float* scratch_f) {
-  double* scratch = reinterpret_cast<double*>(scratch_f);
-  v = warp_sum_d(v);
-  __syncthreads();   // scratch may still be read by the caller's previous phase
-  if ((threadIdx.x & 31) == 0) scratch[threadIdx.x >> 5] = v;
-  __syncthreads();
-  double t = 0.0;
-#pragma unroll
-  for (int w = 0; w < NT / 32; ++w) t += scratch[w];
-  __syncthreads();
-  return t;
-}
-
 __device__ __forceinline__ void softmax_inplace(float* S, int nk) {
   const int lane = threadIdx.x & 31;
   float mx = -INFINITY;
@@ -416,42 +399,6 @@ __global__ void __launch_bounds__(NT) attn_decode_kernel(DecAttnArgs a, float qs
     for (int i = 0; i < VEC; ++i) red[grp * dk + ch * VEC + i] = acc[i];
   }
   __syncthreads();
-  if (a.out_f32 && a.ngain) {
-    // folded cross attention + residual + LayerNorm (tensor.py:98-129): the CTA
-    // holds the whole row (one head, dk = d), so norm(x + o) needs no extra
-    // launch.  Same arithmetic as add_norm_kernel: v = x + y, mean in double,
-    // eps on the deviation scale.
-    float* xr = a.nx + (size_t)r * dk;
-    float* vrow = qs;   // q is no longer needed
-    double part = 0.0;
-    for (int e = tid; e < dk; e += NT) {
-      float sum = red[e];
-      for (int gg = 1; gg < groups; ++gg) sum += red[gg * dk + e];
-      const float y = a.out_bias ? sum + a.out_bias[e] : sum;
-      const float v = xr[e] + y;
-      vrow[e] = v;
-      part += (double)v;
-    }
-    const double tot = block_sum_d<NT>(part, S);   // scores are done; S is 8-byte aligned
-    const float mu = (float)(tot / (double)dk);
-    double qd = 0.0;
-    for (int e = tid; e < dk; e += NT) {
-      const float dv = vrow[e] - mu;
-      vrow[e] = dv;
-      qd += a.nl1 ? (double)fabsf(dv) : (double)(dv * dv);
-    }
-    const double qt = block_sum_d<NT>(qd, S);
-    float sc = (float)(qt / (double)dk);
-    if (!a.nl1) sc = sqrtf(sc);
-    const float den = sc + 1e-6f;
-    T* xa = reinterpret_cast<T*>(a.nx_act) + (size_t)r * dk;
-    for (int e = tid; e < dk; e += NT) {
-      const float o = a.ngain[e] * vrow[e] / den + a.nbeta[e];
-      xr[e] = o;
-      if (a.nx_act) xa[e] = from_f32<T>(o);
-    }
-    return;
-  }
   if (a.out_f32) {   // folded cross attention: o-projection output in fp32 (+ its bias)
     float* out = reinterpret_cast<float*>(a.out) + (size_t)r * a.ldo + h * dk;
     for (int e = tid; e < dk; e += NT) {

@@ -113,30 +113,17 @@ int fnmt_linear_add_norm(const void* A, int lda, int a_dtype, const void* W, int
   g.M = M;
   g.N = N;
   g.K = K;
-  if (fnmt::gemm_norm_supported(N, a_dtype)) {
-    g.epi = fnmt::kEpiNorm;
-    g.C = x;
-    g.ldc = N;
-    g.c_dtype = a_dtype;
-    g.C2 = x_act;
-    g.resid = x;
-    g.ld_resid = N;
-    g.ngain = gain;
-    g.nbeta = beta;
-    g.nl1 = l1;
-    return cuda_status(fnmt::launch_gemm(g, s), "fnmt_linear_add_norm");
-  }
-  float* y = nullptr;
-  cudaError_t e = cudaMallocAsync(&y, sizeof(float) * (size_t)M * N, s);
-  if (e != cudaSuccess) return cuda_status(e, "fnmt_linear_add_norm scratch");
-  g.C = y;
+  // x += A.W + b in place (the epilogue reads and writes each element from the
+  // same thread), then the post-norm over the full rows (tensor.py:98-129)
+  g.C = x;
   g.ldc = N;
   g.c_dtype = fnmt::kF32;
-  e = fnmt::launch_gemm(g, s);
+  g.resid = x;
+  g.ld_resid = N;
+  cudaError_t e = fnmt::launch_gemm(g, s);
   if (e == cudaSuccess)
-    e = fnmt::launch_add_norm(x, y, gain, beta, l1, x, x_act, a_dtype, M, N, s);
-  cudaError_t e2 = cudaFreeAsync(y, s);
-  return cuda_status(e != cudaSuccess ? e : e2, "fnmt_linear_add_norm");
+    e = fnmt::launch_add_norm(x, nullptr, gain, beta, l1, x, x_act, a_dtype, M, N, s);
+  return cuda_status(e, "fnmt_linear_add_norm");
 }
 
 int64_t fnmt_qgemm_workspace(int64_t M, int K) {

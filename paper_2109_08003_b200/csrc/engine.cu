@@ -479,19 +479,6 @@ Lin Engine::make_folded_cross(const std::string& p) {
   return L;
 }
 
-// Opt-in (FNMT_FOLD_NORM=1): residual + norm2 inside the folded cross attention kernel.
-// Correct (143 GPU tests, config-1 fp16 64/64) but r01 measured it neutral-to-slower
-// (6.94M vs 7.03M words/s): the launch it saves is hidden by the concurrent decode lanes
-// while the two block reductions lengthen the attention CTA.
-bool fold_norm_enabled() {
-  static int on = -1;
-  if (on < 0) {
-    const char* e = getenv("FNMT_FOLD_NORM");
-    on = e && e[0] == '1';
-  }
-  return on != 0;
-}
-
 bool fused_cross_enabled() {
   static int on = -1;
   if (on < 0) {
@@ -659,22 +646,6 @@ void Engine::reserve(int tok_cap, int row_cap, int64_t pool_cap) {
               make_tmap_16(&ws.tm_datt, ws.datt, dt, row_cap, d, d, 128, &err) &&
               make_tmap_16(&ws.tm_dh, ws.dh, dt, row_cap, fd, fd, 128, &err);
     if (!ok) throw EngineError(FNMT_E_CUDA, "workspace TMA descriptor: " + err);
-    // decode-attention K/V maps (box = KC keys x min(dk, 256) dims)
-    // Persistent TMA decode attention (decode_attn.cu) is opt-in (FNMT_DECODE_TMA=1): r01
-    // measured 45 ms vs 26 ms (6-1-1) per 16k sentences — per-item consumer latency
-    // (q load, 4 barriers, 1-warp softmax) dominates once the producer runs ahead.
-    const int dkd = d / arch.n_heads_dec;
-    const char* env = getenv("FNMT_DECODE_TMA");
-    ws.kv_tma = env && env[0] == '1' && !fused_cross && dkd % 8 == 0 &&
-                (dkd <= 256 || dkd % 256 == 0);
-    ws.tm_sk.resize(arch.n_dec_layers);
-    ws.tm_sv.resize(arch.n_dec_layers);
-    ws.tm_ckv.resize(arch.n_dec_layers);
-    for (int l = 0; l < arch.n_dec_layers && ws.kv_tma; ++l) {
-      ws.kv_tma = make_tmap_kv(&ws.tm_sk[l], ws.kc[l], dt, pool_cap, d, d, dkd, &err) &&
-                  make_tmap_kv(&ws.tm_sv[l], ws.vc[l], dt, pool_cap, d, d, dkd, &err) &&
-                  make_tmap_kv(&ws.tm_ckv[l], ws.ckv[l], dt, tok_cap, 2 * d, 2 * d, dkd, &err);
-    }
   }
   ws.bytes = device_bytes - before;
 }
@@ -755,45 +726,14 @@ void Engine::norm(const float* x, const float* y, const Norm& n, float* o32, voi
   ++launches;
 }
 
+// x32 = norm(x32 + A.W + b): GEMM into y32 (fp32), then add_norm.  (r01: the residual
+// add in the GEMM epilogue measured slower, 6.30M vs 6.78M words/s, and a clustered
+// GEMM + LayerNorm epilogue exchanging row statistics over DSMEM 4.23M vs 6.81M: the
+// row-local epilogue serialises behind the 1-deep TMEM double buffer.)
 void Engine::gemm_norm(const void* A, const CUtensorMap* tmA, int lda, const Lin& L, int M,
                        float* x32, void* xa, float* y32, const Norm& n, cudaStream_t s) {
-  if (q8 || dt == kF32 || !gemm_norm_enabled() || !gemm_norm_supported(L.N, dt) ||
-      L.N != arch.d_model) {
-    // (r01: moving the residual add into the GEMM epilogue — x32 += A.W + b in place —
-    // measured slower, 6.30M vs 6.78M words/s: the row-per-thread f32 residual loads
-    // stall the epilogue more than add_norm's coalesced second stream costs)
-    gemm(A, tmA, lda, L, M, y32, L.N, kF32, 0, s);
-    norm(x32, y32, n, x32, xa, M, s);
-    return;
-  }
-  GemmArgs g;
-  g.A = A;
-  g.lda = lda;
-  g.W = L.w;
-  g.ldw = L.K;
-  g.in_dtype = dt;
-  g.bias = L.b;
-  g.M = M;
-  g.N = L.N;
-  g.K = L.K;
-  g.epi = kEpiNorm;
-  g.C = x32;
-  g.ldc = L.N;
-  g.c_dtype = dt;
-  g.C2 = xa;
-  g.resid = x32;
-  g.ld_resid = L.N;
-  g.ngain = n.g;
-  g.nbeta = n.b;
-  g.nl1 = arch.norm_l1;
-  g.tmap_a = tmA;
-  g.tmap_w = &L.tm;
-  const int ev = prof_begin(s);
-  CK(launch_gemm(g, s));
-  prof_end(s, ev, gemm_cls, 2.0 * M * L.N * L.K,
-           (double)M * L.K * dtype_size(dt) + (double)L.N * L.K * dtype_size(dt) +
-               (double)M * L.N * (8.0 + dtype_size(dt)));
-  ++launches;
+  gemm(A, tmA, lda, L, M, y32, L.N, kF32, 0, s);
+  norm(x32, y32, n, x32, xa, M, s);
 }
 
 // Encoder over rows already embedded in ws.x32 / ws.xa (model.py:279-286).
@@ -917,10 +857,7 @@ void Engine::run_step(const StepView& v, cudaStream_t s) {
     a.max_k = v.cap;
     {
       const int ev = prof_begin(s);
-      if (v.ws_caches && ws.kv_tma && !v.anc && tc)
-        CK(launch_attention_decode_tma(a, ws.tm_sk[l], ws.tm_sv[l], 0, 0, s));
-      else
-        CK(launch_attention_decode(a, s));
+      CK(launch_attention_decode(a, s));
       prof_end(s, ev, FNMT_K_ATTN_DEC, 0.0, (double)R * (v.host_t + 1) * 2 * d * es);
     }
     ++launches;
@@ -941,13 +878,6 @@ void Engine::run_step(const StepView& v, cudaStream_t s) {
       c.kc_off = 2 * d;
       c.out_f32 = 1;
       c.out_bias = L.co.b;
-      if (fold_norm_enabled()) {   // + residual + norm2 in the same kernel
-        c.nx = ws.dx32;
-        c.nx_act = ws.dxa;
-        c.ngain = L.n2.g;
-        c.nbeta = L.n2.b;
-        c.nl1 = arch.norm_l1;
-      }
     }
     c.dtype = dt;
     c.heads = arch.n_heads_dec;
@@ -961,16 +891,13 @@ void Engine::run_step(const StepView& v, cudaStream_t s) {
     c.max_k = v.max_k;
     {
       const int ev = prof_begin(s);
-      if (v.ws_caches && ws.kv_tma && tc)
-        CK(launch_attention_decode_tma(c, ws.tm_ckv[l], ws.tm_ckv[l], 0, d, s));
-      else
-        CK(launch_attention_decode(c, s));
+      CK(launch_attention_decode(c, s));
       prof_end(s, ev, FNMT_K_ATTN_DEC, 0.0, (double)R * v.max_k * 2 * d * es);
     }
     ++launches;
-    if (folded) {
-      if (!c.ngain) norm(ws.dx32, ws.dy32, L.n2, ws.dx32, ws.dxa, R, s);
-    } else
+    if (folded)
+      norm(ws.dx32, ws.dy32, L.n2, ws.dx32, ws.dxa, R, s);
+    else
       gemm_norm(ws.datt, tc ? &ws.tm_datt : nullptr, d, L.co, R, ws.dx32, ws.dxa, ws.dy32, L.n2, s);
     if (L.ffn) {
       gemm(ws.dxa, tc ? &ws.tm_dxa : nullptr, d, L.f1, R, ws.dh, arch.ffn_dim_dec, dt, 1, s);

@@ -85,9 +85,6 @@ struct Workspace {
   uint8_t* finished = nullptr;
   CUtensorMap tm_xa, tm_att, tm_h, tm_dxa, tm_datt, tm_dh;
   QScratch qs{};   // int8 engines: quantized activations of the current GEMM
-  // decode attention K/V tiles (16-bit caches): self K, self V, cross K|V per layer
-  std::vector<CUtensorMap> tm_sk, tm_sv, tm_ckv;
-  bool kv_tma = false;
 };
 
 struct StepView {
@@ -241,8 +238,7 @@ class Engine {
                    unsigned long long* keys, cudaStream_t s);
   void norm(const float* x, const float* y, const Norm& n, float* o32, void* oa, int rows,
             cudaStream_t s);
-  // x32 = norm(x32 + A.W + b) (and its storage-dtype copy xa): one clustered
-  // GEMM with the LayerNorm in the epilogue when possible, else GEMM + add_norm.
+  // x32 = norm(x32 + A.W + b) (and its storage-dtype copy xa): GEMM + add_norm.
   void gemm_norm(const void* A, const CUtensorMap* tmA, int lda, const Lin& L, int M, float* x32,
                  void* xa, float* y32, const Norm& n, cudaStream_t s);
   void encoder_layers(int n_tok, int n_seq, int max_q, int max_k, const int32_t* qstart,

@@ -63,11 +63,6 @@ struct EpiParams {
   const int32_t* rowsum;
   const unsigned int* stats;
   int qk;
-  // kEpiNorm
-  const float* ngain;
-  const float* nbeta;
-  int nl1;
-  void* C2;
 };
 
 // kEpiQKV destination of output element (m, n): q columns go to C, k / v
@@ -266,119 +261,11 @@ __device__ __forceinline__ void q_dequant_chunk(const EpiParams& ep, int m, floa
 constexpr int kEpiWarps = 8;                       // 2 per TMEM lane quarter
 constexpr int kTcThreads = 64 + kEpiWarps * 32;    // producer + MMA warps, epilogue
 
-// Cluster row-statistic all-reduce for kEpiNorm: every CTA of the cluster
-// contributes one double per row (its BN columns), written into slot `rank`
-// of every peer; each CTA then sums the CN slots in rank order, so all CTAs
-// (and every run, whatever M) get bit-identical statistics.  `bar` expects CN
-// arrivals per use (one per CTA, released after that CTA's stores).
-template <int CN>
-__device__ __forceinline__ double cluster_row_sum(double part_half, int row, int half,
-                                                  double* slots, double* halfbuf, uint64_t* bar,
-                                                  uint32_t parity) {
-  halfbuf[half * kBM + row] = part_half;
-  named_bar_sync(1, kEpiWarps * 32);
-  if (half == 0) {
-    const double part = halfbuf[row] + halfbuf[kBM + row];
-    const uint32_t me = cluster_ctarank();
-    const uint32_t a = smem_u32(slots + me * kBM + row);
-#pragma unroll
-    for (int k = 0; k < CN; ++k) st_cluster_f64(mapa_shared(a, k), part);
-    fence_cluster();
-  }
-  named_bar_sync(1, kEpiWarps * 32);
-  if (threadIdx.x == 64) {
-#pragma unroll
-    for (int k = 0; k < CN; ++k) mbar_arrive_cluster(mapa_shared(smem_u32(bar), k));
-  }
-  mbar_wait_cluster(bar, parity);
-  double tot = 0.0;
-#pragma unroll
-  for (int k = 0; k < CN; ++k) tot += slots[k * kBM + row];
-  return tot;
-}
-
-// out = gain * (v - mu) / (sigma + 1e-6) + beta, v = resid + (acc + bias)
-// (tensor.py:98-129; mean in double, eps added to sigma).  Each thread holds
-// its row's BN/2 columns in registers across both statistic passes.
-template <int BN, int CN>
-__device__ __forceinline__ void norm_epilogue(const EpiParams& ep, uint32_t taddr, const float* bs,
-                                              int m, bool row_ok, int n0, int row, int half, int it,
-                                              double* nslot, double* nhalf, uint64_t* nbar) {
-  constexpr int HC = BN / 2;
-  float v[HC];
-#pragma unroll
-  for (int c = 0; c < HC / 32; ++c) {
-    float t[32];
-    tmem_ld32(taddr + c * 32, t);
-#pragma unroll
-    for (int i = 0; i < 32; ++i) v[c * 32 + i] = t[i] + bs[c * 32 + i];
-  }
-  if (row_ok) {
-    const float* rr = ep.resid + (size_t)m * ep.ld_resid + n0;
-#pragma unroll
-    for (int i = 0; i < HC; i += 4) {
-      const float4 r4 = *reinterpret_cast<const float4*>(rr + i);
-      v[i] = r4.x + v[i];
-      v[i + 1] = r4.y + v[i + 1];
-      v[i + 2] = r4.z + v[i + 2];
-      v[i + 3] = r4.w + v[i + 3];
-    }
-  } else {
-#pragma unroll
-    for (int i = 0; i < HC; ++i) v[i] = 0.f;
-  }
-  const int par = it & 1;
-  const uint32_t use = (uint32_t)(it >> 1) & 1u;
-  double* slots = nslot + (size_t)par * 2 * CN * kBM;
-  double s = 0.0;
-#pragma unroll
-  for (int i = 0; i < HC; ++i) s += (double)v[i];
-  s = cluster_row_sum<CN>(s, row, half, slots, nhalf, nbar + 2 * par, use);
-  const int d = ep.N;
-  const float mu = (float)(s / (double)d);
-  double q = 0.0;
-#pragma unroll
-  for (int i = 0; i < HC; ++i) {
-    v[i] -= mu;
-    q += ep.nl1 ? (double)fabsf(v[i]) : (double)(v[i] * v[i]);
-  }
-  named_bar_sync(1, kEpiWarps * 32);   // halves finished reading nhalf of pass 1
-  q = cluster_row_sum<CN>(q, row, half, slots + CN * kBM, nhalf, nbar + 2 * par + 1, use);
-  float sc = (float)(q / (double)d);
-  if (!ep.nl1) sc = sqrtf(sc);
-  const float den = sc + 1e-6f;
-  if (!row_ok) return;
-  float* o32 = reinterpret_cast<float*>(ep.C) + (size_t)m * ep.ldc + n0;
-#pragma unroll
-  for (int i = 0; i < HC; i += 4) {
-    float4 o;
-    o.x = ep.ngain[n0 + i] * v[i] / den + ep.nbeta[n0 + i];
-    o.y = ep.ngain[n0 + i + 1] * v[i + 1] / den + ep.nbeta[n0 + i + 1];
-    o.z = ep.ngain[n0 + i + 2] * v[i + 2] / den + ep.nbeta[n0 + i + 2];
-    o.w = ep.ngain[n0 + i + 3] * v[i + 3] / den + ep.nbeta[n0 + i + 3];
-    *reinterpret_cast<float4*>(o32 + i) = o;
-    if (ep.C2) {
-      uint32_t p0, p1;
-      if (ep.c_dtype == kF16) {
-        __half2 a = __floats2half2_rn(o.x, o.y), b = __floats2half2_rn(o.z, o.w);
-        p0 = *reinterpret_cast<uint32_t*>(&a);
-        p1 = *reinterpret_cast<uint32_t*>(&b);
-      } else {
-        __nv_bfloat162 a = __floats2bfloat162_rn(o.x, o.y), b = __floats2bfloat162_rn(o.z, o.w);
-        p0 = *reinterpret_cast<uint32_t*>(&a);
-        p1 = *reinterpret_cast<uint32_t*>(&b);
-      }
-      *reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(ep.C2) + (size_t)m * ep.ldc + n0 + i) =
-          make_uint2(p0, p1);
-    }
-  }
-}
-
 // ---------------------------------------------------------------------------
 // persistent tcgen05 kernel
 
 // Every stage row is 128 bytes of K: 64 fp16/bf16 elements, or 128 int8.
-template <int BN, int STAGES, bool I8 = false, int CN = 0, int TK = 0>
+template <int BN, int STAGES, bool I8 = false, int TK = 0>
 struct TcCfg {
   // TK (beam top-K epilogue): per-row exchange of the two column halves' partials
   static constexpr int kTkBytes = TK ? kBM * (4 + 8 + 8 * TK) : 0;
@@ -387,25 +274,13 @@ struct TcCfg {
   static constexpr int kStage = kABytes + kBBytes;
   static constexpr int kTmemCols = 2 * BN;   // double-buffered accumulator
   static constexpr int kColBytes = I8 ? 16 : 4;   // bias (+ scale, zeropoint, column sum)
-  // kEpiNorm: row-statistic slots [parity][pass][rank][128] + half-row partials [2][128]
-  static constexpr int kNormBytes = CN ? (4 * CN * kBM + 2 * kBM) * 8 + 64 : 0;
-  static constexpr int kSmem =
-      1024 + STAGES * kStage + 2 * BN * kColBytes + kNormBytes + kTkBytes + 256;
+  static constexpr int kSmem = 1024 + STAGES * kStage + 2 * BN * kColBytes + kTkBytes + 256;
 };
 
-// Tile of this CTA's it-th iteration (-1 when done).  Plain: a grid-stride
-// walk.  Clustered (CN > 0, kEpiNorm): the CN CTAs of a cluster take the CN
-// N tiles of the same 128-row block, block after block.
-template <int CN>
-__device__ __forceinline__ int tile_at(int it, int tiles, int tiles_n) {
-  if constexpr (CN == 0) {
-    const int t = blockIdx.x + it * gridDim.x;
-    return t < tiles ? t : -1;
-  } else {
-    const int ncl = gridDim.x / CN;
-    const int mb = blockIdx.x / CN + it * ncl;
-    return mb < tiles / tiles_n ? mb * tiles_n + (int)(blockIdx.x % CN) : -1;
-  }
+// Tile of this CTA's it-th iteration (-1 when done): a grid-stride walk.
+__device__ __forceinline__ int tile_at(int it, int tiles) {
+  const int t = blockIdx.x + it * gridDim.x;
+  return t < tiles ? t : -1;
 }
 
 
@@ -522,11 +397,11 @@ __device__ __forceinline__ void topk_epilogue(const EpiParams& ep, uint32_t tadd
   }
 }
 
-template <int BN, int STAGES, int TOPK, bool I8 = false, int MINB = 1, int CN = 0>
+template <int BN, int STAGES, int TOPK, bool I8 = false, int MINB = 1>
 __global__ void __launch_bounds__(kTcThreads, MINB)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmw,
                    int K, uint32_t idesc, EpiParams ep, int tiles_n, int tiles) {
-  using Cfg = TcCfg<BN, STAGES, I8, CN, TOPK>;
+  using Cfg = TcCfg<BN, STAGES, I8, TOPK>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -537,11 +412,8 @@ __global__ void __launch_bounds__(kTcThreads, MINB)
   float* qsc_s = bias_s + 2 * BN;
   float* qzp_s = qsc_s + (I8 ? 2 * BN : 0);
   int32_t* qcs_s = reinterpret_cast<int32_t*>(qzp_s + (I8 ? 2 * BN : 0));
-  // kEpiNorm slots (8-byte aligned: everything before is a multiple of 8 bytes)
-  double* nslot = reinterpret_cast<double*>(bias_s + (Cfg::kColBytes / 4) * 2 * BN);
-  double* nhalf = nslot + (CN ? 4 * CN * kBM : 0);
-  uint64_t* nbar = reinterpret_cast<uint64_t*>(nhalf + (CN ? 2 * kBM : 0));   // [parity][pass]
-  uint8_t* tks = reinterpret_cast<uint8_t*>(nbar + (CN ? 4 : 0));   // TOPK: half exchange
+  // TOPK: half exchange (8-byte aligned: everything before is a multiple of 8 bytes)
+  uint8_t* tks = reinterpret_cast<uint8_t*>(bias_s + (Cfg::kColBytes / 4) * 2 * BN);
   uint64_t* full = reinterpret_cast<uint64_t*>(tks + Cfg::kTkBytes);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
@@ -563,14 +435,11 @@ __global__ void __launch_bounds__(kTcThreads, MINB)
       mbar_init(tfull + b, 1);
       mbar_init(tempty + b, kEpiWarps);
     }
-    if constexpr (CN > 0)
-      for (int b = 0; b < 4; ++b) mbar_init(nbar + b, CN);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc(tslot, Cfg::kTmemCols);
   tc_fence_before();
   __syncthreads();
-  if constexpr (CN > 0) cluster_sync_all();   // peers' barriers initialised before any remote arrive
   tc_fence_after();
   const uint32_t tmem = *tslot;
   // PDL: barrier init / TMEM alloc / descriptor prefetch above overlap the
@@ -583,7 +452,7 @@ __global__ void __launch_bounds__(kTcThreads, MINB)
       int s = 0;
       uint32_t ph = 0;
       for (int it = 0;; ++it) {
-        const int tile = tile_at<CN>(it, tiles, tiles_n);
+        const int tile = tile_at(it, tiles);
         if (tile < 0) break;
         const int m0 = (tile / tiles_n) * kBM;
         const int n0 = (tile % tiles_n) * BN;
@@ -609,7 +478,7 @@ __global__ void __launch_bounds__(kTcThreads, MINB)
       int acc = 0;
       uint32_t aph = 0;
       for (int it = 0;; ++it) {
-        if (tile_at<CN>(it, tiles, tiles_n) < 0) break;
+        if (tile_at(it, tiles) < 0) break;
         mbar_wait(tempty + acc, aph ^ 1);
         tc_fence_after();
         const uint32_t d = tmem + acc * BN;
@@ -645,7 +514,7 @@ __global__ void __launch_bounds__(kTcThreads, MINB)
     int acc = 0;
     uint32_t aph = 0;
     for (int it = 0;; ++it) {
-      const int tile = tile_at<CN>(it, tiles, tiles_n);
+      const int tile = tile_at(it, tiles);
       if (tile < 0) break;
       const int m0 = (tile / tiles_n) * kBM;
       const int n0 = (tile % tiles_n) * BN;
@@ -667,13 +536,7 @@ __global__ void __launch_bounds__(kTcThreads, MINB)
       const bool row_ok = m < ep.M;
       const int col0 = half * (BN / 2);
       const uint32_t taddr = tmem + acc * BN + col0 + ((uint32_t)(quarter * 32) << 16);
-      if constexpr (CN > 0) {
-        norm_epilogue<BN, CN>(ep, taddr, bs + col0, m, row_ok, n0 + col0, quarter * 32 + lane,
-                              half, it, nslot, nhalf, nbar);
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(tempty + acc);
-      } else if constexpr (TOPK > 0) {
+      if constexpr (TOPK > 0) {
         topk_epilogue<BN, TOPK>(ep, taddr, bs + col0, m, row_ok, n0 + col0, half,
                                 quarter * 32 + lane, tks);
         tc_fence_before();
@@ -708,7 +571,6 @@ __global__ void __launch_bounds__(kTcThreads, MINB)
   }
   tc_fence_before();
   __syncthreads();
-  if constexpr (CN > 0) cluster_sync_all();   // no CTA leaves while peers may still signal it
   if (warp == 1) tmem_dealloc(tmem, Cfg::kTmemCols);
 }
 
@@ -801,7 +663,7 @@ int num_sms() {
 template <int BN, int STAGES, int TOPK = 0, bool I8 = false, int MINB = 1>
 cudaError_t launch_tc(const CUtensorMap& ta, const CUtensorMap& tw, const GemmArgs& g,
                       const EpiParams& ep, cudaStream_t s) {
-  using Cfg = TcCfg<BN, STAGES, I8, 0, TOPK>;
+  using Cfg = TcCfg<BN, STAGES, I8, TOPK>;
   static_assert(Cfg::kSmem <= 227 * 1024, "GEMM stage ring exceeds shared memory");
   static_assert(MINB == 1 || MINB * (Cfg::kSmem + 1024) <= 228 * 1024, "MINB CTAs do not fit");
   auto kern = gemm_tc_kernel<BN, STAGES, TOPK, I8, MINB>;
@@ -816,259 +678,9 @@ cudaError_t launch_tc(const CUtensorMap& ta, const CUtensorMap& tw, const GemmAr
 }
 
 
-// ---------------------------------------------------------------------------
-// CTA-pair kernel (cta_group::2): a 256 x BN tile per cluster of 2 CTAs.
-// Each CTA stages its own 128 rows of A and BN/2 rows of W^T per k-block
-// (TMA completions counted on the leader's barrier); the leader's single
-// thread issues tcgen05.mma.cta_group::2 (M = 256) which reads both CTAs'
-// smem and accumulates each CTA's 128 rows x BN in its own TMEM; commits are
-// multicast to both CTAs.  Per CTA and k-block: 16 KB of A + BN/2 x 128 B of
-// W for 2 x 128 x BN x 64 FLOP — a third less L2 traffic per FLOP than the
-// single-CTA 128 x BN tile.  Epilogues are the single-CTA ones.
-template <int BN, int STAGES>
-struct Tc2Cfg {
-  static constexpr int kBHalf = BN / 2;
-  static constexpr int kBBytes = kBHalf * kBK * 2;
-  static constexpr int kStage = kABytes + kBBytes;
-  static constexpr int kTmemCols = 2 * BN;
-  static constexpr int kSmem = 1024 + STAGES * kStage + 2 * BN * 4 + 256;
-};
-
-template <int BN, int STAGES>
-__global__ void __launch_bounds__(kTcThreads, 1)
-    gemm_tc2_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmw,
-                    int K, uint32_t idesc, EpiParams ep, int tiles_n, int tiles) {
-  using Cfg = Tc2Cfg<BN, STAGES>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~static_cast<uintptr_t>(1023));
-  uint8_t* sA = base;
-  uint8_t* sB = base + STAGES * kABytes;
-  float* bias_s = reinterpret_cast<float*>(sB + STAGES * Cfg::kBBytes);   // [2][BN]
-  uint64_t* full = reinterpret_cast<uint64_t*>(bias_s + 2 * BN);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
-
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  const uint32_t rank = cluster_ctarank();
-  const bool leader = rank == 0;
-  const int ncl = gridDim.x / 2, cid = blockIdx.x / 2;
-  const int nk = (K + kBK - 1) / kBK;
-
-  if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(&tma);
-    tma_prefetch_desc(&tmw);
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(full + s, 1);
-      mbar_init(empty + s, 1);
-    }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(tfull + b, 1);
-      mbar_init(tempty + b, 2 * kEpiWarps);   // both CTAs' epilogue warps release it
-    }
-    fence_mbar_init();
-  }
-  if (warp == 1) tmem_alloc_pair(tslot, Cfg::kTmemCols);
-  tc_fence_before();
-  __syncthreads();
-  cluster_sync_all();   // barriers of both CTAs initialised, TMEM of the pair allocated
-  tc_fence_after();
-  const uint32_t tmem = *tslot;
-  pdl_trigger();
-  pdl_wait();
-
-  if (warp == 0) {
-    if (lane == 0) {
-      int s = 0;
-      uint32_t ph = 0;
-      for (int tile = cid; tile < tiles; tile += ncl) {
-        const int m0 = (tile / tiles_n) * 2 * kBM + rank * kBM;
-        const int n0 = (tile % tiles_n) * BN + rank * Cfg::kBHalf;
-        for (int kb = 0; kb < nk; ++kb) {
-          mbar_wait(empty + s, ph ^ 1);
-          if (leader) mbar_expect_tx(full + s, 2 * Cfg::kStage);
-          tma_load_2d_pair(sA + s * kABytes, &tma, full + s, kb * kBK, m0);
-#pragma unroll
-          for (int j = 0; j < Cfg::kBHalf / kWBox; ++j)
-            tma_load_2d_pair(sB + s * Cfg::kBBytes + j * kWBox * 128, &tmw, full + s, kb * kBK,
-                             n0 + j * kWBox);
-          if (++s == STAGES) {
-            s = 0;
-            ph ^= 1;
-          }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    if (leader && lane == 0) {
-      int s = 0;
-      uint32_t ph = 0;
-      int acc = 0;
-      uint32_t aph = 0;
-      for (int tile = cid; tile < tiles; tile += ncl) {
-        mbar_wait(tempty + acc, aph ^ 1);
-        tc_fence_after();
-        const uint32_t d = tmem + acc * BN;
-        for (int kb = 0; kb < nk; ++kb) {
-          mbar_wait(full + s, ph);
-          tc_fence_after();
-          const uint64_t ad = umma_desc_sw128(smem_u32(sA + s * kABytes));
-          const uint64_t bd = umma_desc_sw128(smem_u32(sB + s * Cfg::kBBytes));
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk)
-            tc_mma_f16_pair(d, ad + 2 * kk, bd + 2 * kk, idesc, (kb | kk) != 0 ? 1u : 0u);
-          tc_commit_pair(empty + s);
-          if (++s == STAGES) {
-            s = 0;
-            ph ^= 1;
-          }
-        }
-        tc_commit_pair(tfull + acc);
-        acc ^= 1;
-        if (acc == 0) aph ^= 1;
-      }
-    }
-  } else {
-    const int quarter = warp & 3;
-    const int half = (warp - 2) >> 2;
-    const uint32_t tempty_leader0 = mapa_shared(smem_u32(tempty), 0);
-    int acc = 0;
-    uint32_t aph = 0;
-    for (int tile = cid; tile < tiles; tile += ncl) {
-      const int m0 = (tile / tiles_n) * 2 * kBM + rank * kBM;
-      const int n0 = (tile % tiles_n) * BN;
-      float* bs = bias_s + acc * BN;
-      for (int i = threadIdx.x - 64; i < BN; i += kEpiWarps * 32)
-        bs[i] = (ep.bias && n0 + i < ep.N) ? ep.bias[n0 + i] : 0.f;
-      named_bar_sync(1, kEpiWarps * 32);
-      mbar_wait(tfull + acc, aph);
-      tc_fence_after();
-      const int m = m0 + quarter * 32 + lane;
-      const bool row_ok = m < ep.M;
-      const int col0 = half * (BN / 2);
-      const uint32_t taddr = tmem + acc * BN + col0 + ((uint32_t)(quarter * 32) << 16);
-      float best_v = -INFINITY;
-      int best_i = -1;
-#pragma unroll 1
-      for (int c = 0; c < BN / 64; ++c) {
-        float v[32];
-        tmem_ld32(taddr + c * 32, v);
-        const int nb = n0 + col0 + c * 32;
-        if (row_ok && nb < ep.N) epilogue_chunk(ep, m, nb, v, bs + col0 + c * 32, best_v, best_i);
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(tempty_leader0 + (uint32_t)(acc * 8));
-      if (ep.epi == kEpiArgmax && row_ok && best_i >= 0)
-        atomicMax(ep.keys + m, argmax_key(best_v, (uint32_t)best_i));
-      acc ^= 1;
-      if (acc == 0) aph ^= 1;
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  cluster_sync_all();   // the peer's MMAs / arrives are done before TMEM goes away
-  if (warp == 1) tmem_dealloc_pair(tmem, Cfg::kTmemCols);
-}
-
-template <int BN, int STAGES>
-cudaError_t launch_tc2(const CUtensorMap& ta, const CUtensorMap& tw, const GemmArgs& g,
-                       const EpiParams& ep, cudaStream_t s) {
-  using Cfg = Tc2Cfg<BN, STAGES>;
-  static_assert(Cfg::kSmem <= 227 * 1024, "pair GEMM stage ring exceeds shared memory");
-  auto kern = gemm_tc2_kernel<BN, STAGES>;
-  cudaError_t e = set_max_smem((const void*)kern);
-  if (e != cudaSuccess) return e;
-  const int tiles_n = (g.N + BN - 1) / BN;
-  const int tiles = tiles_n * ((g.M + 2 * kBM - 1) / (2 * kBM));
-  const int pairs = std::min(tiles, num_sms() / 2);
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(2 * pairs);
-  cfg.blockDim = dim3(kTcThreads);
-  cfg.dynamicSmemBytes = Cfg::kSmem;
-  cfg.stream = s;
-  cudaLaunchAttribute at[2];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = 2;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[1].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = pdl_enabled() ? 2 : 1;
-  const uint32_t idesc = umma_idesc_f16(2 * kBM, BN, g.in_dtype == kBF16);
-  return cudaLaunchKernelEx(&cfg, kern, ta, tw, g.K, idesc, ep, tiles_n, tiles);
-}
-
-// kEpiNorm: clusters of CN CTAs along N (one per N tile of a row block).
-template <int BN, int STAGES, int CN>
-cudaError_t launch_tc_norm(const CUtensorMap& ta, const CUtensorMap& tw, const GemmArgs& g,
-                           const EpiParams& ep, cudaStream_t s) {
-  using Cfg = TcCfg<BN, STAGES, false, CN>;
-  static_assert(Cfg::kSmem <= 227 * 1024, "GEMM stage ring exceeds shared memory");
-  auto kern = gemm_tc_kernel<BN, STAGES, 0, false, 1, CN>;
-  cudaError_t e = set_max_smem((const void*)kern);
-  if (e != cudaSuccess) return e;
-  const int tiles_n = CN;
-  const int tiles_m = (g.M + kBM - 1) / kBM;
-  const int clusters = std::min(tiles_m, std::max(1, num_sms() / CN));
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(clusters * CN);
-  cfg.blockDim = dim3(kTcThreads);
-  cfg.dynamicSmemBytes = Cfg::kSmem;
-  cfg.stream = s;
-  cudaLaunchAttribute at[2];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = CN;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[1].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = pdl_enabled() ? 2 : 1;
-  const uint32_t idesc = umma_idesc_f16(kBM, BN, g.in_dtype == kBF16);
-  return cudaLaunchKernelEx(&cfg, kern, ta, tw, g.K, idesc, ep, tiles_n, tiles_m * tiles_n);
-}
-
 }  // namespace
 
-// The engine's post-norm blocks use it only with FNMT_GEMM_NORM=1: r01 measured the
-// clustered epilogue slower than GEMM + add_norm (6-1-1 bench 4.23M vs 6.81M words/s;
-// encoder GEMMs 74 vs 21 ms per 16k sentences) — two DSMEM round trips per 128-row tile
-// serialise the epilogue, which then dominates the 1-tile-deep TMEM double buffer.
-// fnmt_linear_add_norm (C ABI) always fuses.
-bool gemm_norm_enabled() {
-  static int on = -1;
-  if (on < 0) {
-    const char* e = getenv("FNMT_GEMM_NORM");
-    on = e && e[0] == '1';
-  }
-  return on != 0;
-}
-
-bool gemm_norm_supported(int N, int in_dtype) {
-  if (in_dtype != kF16 && in_dtype != kBF16) return false;
-  return N == 256 || N == 512 || N == 768 || N == 1024;
-}
-
 int gemm_tile_n() { return kWBox; }
-
-// CTA-pair (cta_group::2) tiles for the large GEMMs: opt-in (FNMT_GEMM_PAIR=1).  Correct
-// (tests/pair_gemm_check.py) but r01 measured no gain: 6-1-1 bench 6.72M vs 6.82M words/s
-// (vocab 29.3 vs 25.1 ms per 16k sentences, encoder GEMMs equal), Deep beam 4 0.426M vs
-// 0.422M — the single-CTA 128 x 256 tiles are not L2-bandwidth bound at these shapes (the
-// vocab GEMM alone reaches 1479 TFLOP/s at 9216 rows, profiles/r01c_step_analysis.md).
-bool pair_enabled() {
-  static int on = -1;
-  if (on < 0) {
-    const char* e = getenv("FNMT_GEMM_PAIR");
-    on = e && e[0] == '1';
-  }
-  return on != 0;
-}
 
 bool dual_cta_enabled() {
   static int on = -1;
@@ -1114,34 +726,6 @@ bool make_tmap_16(CUtensorMap* out, const void* base, int dtype, int64_t rows, i
   return true;
 }
 
-bool make_tmap_kv(CUtensorMap* out, const void* base, int dtype, int64_t rows, int64_t cols,
-                  int64_t ld, int dk, std::string* err) {
-  auto fn = encode_fn();
-  if (!fn) {
-    if (err) *err = "cuTensorMapEncodeTiled unavailable";
-    return false;
-  }
-  const int bc = dk < 256 ? dk : 256;
-  if ((reinterpret_cast<uintptr_t>(base) & 15) || ((ld * 2) & 15) || ((bc * 2) & 15) ||
-      (dk % bc)) {
-    if (err) *err = "KV tensor map: misaligned base / leading dim / head size";
-    return false;
-  }
-  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
-  cuuint32_t box[2] = {(cuuint32_t)bc, (cuuint32_t)decode_tma_keys_per_chunk(dk, dtype)};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = fn(out, dtype == kBF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
-                  2, const_cast<void*>(base), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) {
-    if (err) *err = "cuTensorMapEncodeTiled (KV) failed with CUresult " + std::to_string((int)r);
-    return false;
-  }
-  return true;
-}
-
 // N tile: the largest of 256/128/64 that still gives >= FNMT_BN_WAVE x SMs
 // tiles (default 0.6: r01 A/B at 9216-row decode steps 740 / 757 / 768 / 798 us
 // for 0.6 / 0.9 / 1.0 / 2.0 — bigger N tiles re-read A less often).
@@ -1165,12 +749,7 @@ cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t s) {
   if (g.qw) return launch_qgemm(g, s);
   EpiParams ep{g.bias, g.M, g.N, g.epi, g.C, g.ldc, g.c_dtype, g.relu, g.resid, g.ld_resid,
                g.keys, g.topk, g.kc, g.vc, g.cap, g.seg, g.t_ptr,
-               nullptr, nullptr, nullptr, nullptr, nullptr, 0,
-               g.ngain, g.nbeta, g.nl1, g.C2};
-  if (g.epi == kEpiNorm &&
-      (!gemm_norm_supported(g.N, g.in_dtype) || !g.resid || !g.ngain || !g.nbeta ||
-       g.ldc != g.N || g.ld_resid != g.N || (g.C2 && g.c_dtype == kF32)))
-    return cudaErrorInvalidValue;
+               nullptr, nullptr, nullptr, nullptr, nullptr, 0};
   if (g.epi == kEpiQKV && (!g.kc || !g.vc || !g.t_ptr || g.seg <= 0 || g.N != 3 * g.seg))
     return cudaErrorInvalidValue;
   if (g.epi == kEpiTopK && (g.in_dtype == kF32 || (g.topk.K != 4 && g.topk.K != 8)))
@@ -1194,22 +773,11 @@ cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t s) {
       return cudaErrorInvalidValue;
     pw = &tw;
   }
-  if (g.epi == kEpiNorm) {
-    switch (g.N) {
-      case 256: return launch_tc_norm<64, 4, 4>(*pa, *pw, g, ep, s);
-      case 512: return launch_tc_norm<64, 4, 8>(*pa, *pw, g, ep, s);
-      case 768: return launch_tc_norm<128, 4, 6>(*pa, *pw, g, ep, s);
-      default: return launch_tc_norm<128, 4, 8>(*pa, *pw, g, ep, s);
-    }
-  }
   if (g.epi == kEpiTopK) {
     static_assert(kTopKTile == 256, "one top-K partial per BN = 256 tile");
     return g.topk.K == 4 ? launch_tc<256, 4, 4>(*pa, *pw, g, ep, s)
                          : launch_tc<256, 4, 8>(*pa, *pw, g, ep, s);
   }
-  if (pair_enabled() && (g.epi == kEpiStore || g.epi == kEpiArgmax) &&
-      (int64_t)((g.M + 2 * kBM - 1) / (2 * kBM)) * ((g.N + 255) / 256) >= num_sms() / 2)
-    return launch_tc2<256, 6>(*pa, *pw, g, ep, s);
   switch (pick_bn(g.M, g.N)) {
     case 256: return launch_tc<256, 4>(*pa, *pw, g, ep, s);
     case 128: return launch_tc<128, 6>(*pa, *pw, g, ep, s);
@@ -1222,11 +790,9 @@ cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t s) {
 // int8 tcgen05 GEMM over activations already quantized into g.qs (qgemm.cu).
 cudaError_t launch_tc_i8(const CUtensorMap& ta, const GemmArgs& g, cudaStream_t s) {
   if (g.epi == kEpiTopK || !g.qtmap_w) return cudaErrorInvalidValue;
-  if (g.epi == kEpiNorm) return cudaErrorInvalidValue;
   EpiParams ep{g.bias, g.M, g.N, g.epi, g.C, g.ldc, g.c_dtype, g.relu, g.resid, g.ld_resid,
                g.keys, g.topk, g.kc, g.vc, g.cap, g.seg, g.t_ptr,
-               g.qscale, g.qzp, g.qcolsum, g.qs.rowsum, g.qs.stats, g.K,
-               nullptr, nullptr, 0, nullptr};
+               g.qscale, g.qzp, g.qcolsum, g.qs.rowsum, g.qs.stats, g.K};
   switch (pick_bn(g.M, g.N)) {
     case 256: return launch_tc<256, 4, 0, true>(ta, *g.qtmap_w, g, ep, s);
     case 128: return launch_tc<128, 6, 0, true>(ta, *g.qtmap_w, g, ep, s);

@@ -31,7 +31,6 @@ inline cudaError_t set_max_smem(const void* func) {
 // their predecessor's data (common.cuh).
 bool pdl_enabled();
 bool dual_cta_enabled();   // FNMT_GEMM_DUAL=0 disables 2-CTA/SM decoder GEMMs
-bool pair_enabled();       // FNMT_GEMM_PAIR=1: cta_group::2 256-row tiles for large GEMMs
 template <typename... KArgs, typename... Args>
 cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                      Args&&... args) {
@@ -54,9 +53,6 @@ enum Epilogue : int {
   kEpiArgmax = 1,  // keys[m] = max over n < valid_n of key(acc + bias[n], n)
   kEpiTopK = 2,    // per (row, 256-column tile): max, sum exp(x - max), top-K (value, index)
   kEpiQKV = 3,     // decoder self q|k|v: q -> C, k / v -> KV cache slot (row*cap + *t_ptr)
-  kEpiNorm = 4,    // out = norm(resid + acc + bias) * gain + beta over the full row: the N
-                   // tiles of a row block live in one thread-block cluster and exchange
-                   // row statistics through distributed shared memory
 };
 
 // Per-(row, N-tile) partials of the beam epilogue; tile = n / kTopKTile.
@@ -125,18 +121,7 @@ struct GemmArgs {
   int Kp = 0;
   const CUtensorMap* qtmap_w = nullptr;
   QScratch qs{};
-  // kEpiNorm (model.py:193-196 after the residual add, tensor.py:98-129):
-  // resid is the f32 residual stream x, C the f32 output (may alias resid),
-  // C2 the storage-dtype copy (c_dtype) for the next GEMM.
-  const float* ngain = nullptr;
-  const float* nbeta = nullptr;
-  int nl1 = 0;
-  void* C2 = nullptr;
 };
-// Can launch_gemm fuse the LayerNorm for this (N, dtype)?  (tensor-core path,
-// N = cluster size x N tile with cluster size <= 8)
-bool gemm_norm_supported(int N, int in_dtype);
-bool gemm_norm_enabled();   // engine opt-in (FNMT_GEMM_NORM=1)
 
 // Encode a 2-D TMA descriptor for a row-major [rows, cols] 16-bit matrix with
 // leading dimension ld (elements), box = [box_rows, 64 cols], 128 B swizzle.
@@ -214,26 +199,8 @@ struct DecAttnArgs {
   int kc_off = -1;
   const float* out_bias = nullptr;
   int out_f32 = 0;
-  // ... and optionally the post-norm block fused in (single head, row = dk):
-  // x[r] = norm(x[r] + out) * gain + beta in place (fp32), copy in T to x_act
-  float* nx = nullptr;
-  void* nx_act = nullptr;
-  const float* ngain = nullptr;
-  const float* nbeta = nullptr;
-  int nl1 = 0;
 };
 cudaError_t launch_attention_decode(const DecAttnArgs& a, cudaStream_t s);
-
-// TMA-fed variant (16-bit caches, no ancestor table): K/V tiles of KC keys
-// x min(dk, 256) columns are streamed through a 3-stage smem ring by 2-D
-// tensor maps `tk` / `tv` (rows = cache rows, cols = model dims); the key
-// columns of head h start at k_col0 + h*dk, values at v_col0 + h*dk.
-int decode_tma_keys_per_chunk(int dk, int dtype);
-bool make_tmap_kv(CUtensorMap* out, const void* base, int dtype, int64_t rows, int64_t cols,
-                  int64_t ld, int dk, std::string* err);
-cudaError_t launch_attention_decode_tma(const DecAttnArgs& a, const CUtensorMap& tk,
-                                        const CUtensorMap& tv, int k_col0, int v_col0,
-                                        cudaStream_t s);
 
 // ---------------------------------------------------------------------------
 // search bookkeeping (search.py:58-86)

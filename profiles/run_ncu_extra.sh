@@ -9,7 +9,7 @@ export FNMT_LANES=1
 run() {  # name kernel-regex skip count profile_step-args...
   local name=$1 pat=$2 skip=$3 cnt=$4; shift 4
   ncu --set full --clock-control none -k "regex:$pat" --launch-skip $skip --launch-count $cnt \
-      -o gpurun_out/full_${R}_$name python -m paper_2109_08003_b200.profile_step "$@" \
+      -o gpurun_out/full_${R}_$name python tools/profile_step.py "$@" \
       > gpurun_out/ncu_full_${R}_$name.log 2>&1
   ncu -i gpurun_out/full_${R}_$name.ncu-rep --page raw --csv > gpurun_out/full_${R}_$name.csv 2>/dev/null
   gzip -f gpurun_out/full_${R}_$name.csv

@@ -105,18 +105,3 @@ def test_beam1_equals_greedy_native(golden):
         g1 = greedy_translate(m, enc, SearchConfig(2, 3, 0))
         b1 = beam_translate(m, enc, SearchConfig(2, 3, 0, beam_size=1))
         assert g1 == b1, seed
-
-
-def test_decode_tma_path():
-    """The opt-in TMA-fed persistent decode attention (FNMT_DECODE_TMA=1) on
-    Student-6-1-8 against the reference beam fixtures, in a subprocess (the
-    switch is read at workspace reservation; a hang cannot stall the suite)."""
-    import os
-    import subprocess
-    import sys
-    from pathlib import Path
-    env = dict(os.environ, FNMT_DECODE_TMA="1")
-    r = subprocess.run([sys.executable, str(Path(__file__).parent / "decode_tma_check.py")],
-                       env=env, capture_output=True, text=True, timeout=300)
-    assert r.returncode == 0, r.stdout + r.stderr
-    assert "decode tma ok" in r.stdout

@@ -259,20 +259,6 @@ def test_folded_cross_attention_corpus_path(dtype):
         assert rep["all_near_ties"], (k, rep)
 
 
-def test_fold_norm_path():
-    """Opt-in FNMT_FOLD_NORM=1 (residual + norm2 inside the folded cross
-    attention) on BASELINE config 1, in a subprocess (the switch is read once)."""
-    import os
-    import subprocess
-    import sys
-    from pathlib import Path
-    env = dict(os.environ, FNMT_FOLD_NORM="1")
-    r = subprocess.run([sys.executable, str(Path(__file__).parent / "fold_norm_check.py")],
-                       env=env, capture_output=True, text=True, timeout=300)
-    assert r.returncode == 0, r.stdout + r.stderr
-    assert "fold norm ok" in r.stdout
-
-
 def test_engine_translate_absolute_offsets(golden):
     """fnmt_engine_translate reads sentence i at ids[offsets[i]:offsets[i+1]]
     with absolute offsets into the caller's array (include/fnmt_b200.h): a

@@ -1,6 +1,10 @@
 """Debug probe: translate each 65536-sentence chunk of the bench corpus
 through Engine.translate_device (as bench.py does) and report progress, to
-find chunks that fail.  Usage: python -m paper_2109_08003_b200.chunk_probe [first last]"""
+find chunks that fail.  Usage: python tools/chunk_probe.py [first last]"""
+
+import sys
+from pathlib import Path
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 import sys
 
 import numpy as np

@@ -1,14 +1,18 @@
 """GEMM shape microbenchmark for the tcgen05 kernel (fnmt_linear), warm L2,
 launches captured in a CUDA graph and timed with CUDA events.
 
-python -m paper_2109_08003_b200.perf_gemm
+python tools/perf_gemm.py
 """
+
+import sys
+from pathlib import Path
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 import sys
 
 import torch
 
-from . import _capi
-from ._capi import check, lib, ptr
+from paper_2109_08003_b200 import _capi
+from paper_2109_08003_b200._capi import check, lib, ptr
 
 SHAPES = [  # (M, N, K, note)
     (600, 512, 512, "dec o-proj, long batch"),

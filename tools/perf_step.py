@@ -3,7 +3,11 @@
 the engine's own decode time / step count, to set against the sum of the
 step's kernel durations from an ncu launch list of the same command.
 
-Usage: python -m paper_2109_08003_b200.perf_step [rows] [src_len] [lanes] [sbatch]"""
+Usage: python tools/perf_step.py [rows] [src_len] [lanes] [sbatch]"""
+
+import sys
+from pathlib import Path
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 import os
 import sys
 

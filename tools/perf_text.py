@@ -2,7 +2,11 @@
 engine -> detokenize) for Student-6-1-1 fp16 on a synthetic corpus: lines of
 newstest-shaped length whose words are Zipf-distributed vocabulary tokens.
 
-Usage: python -m paper_2109_08003_b200.perf_text [n_lines] [workers]"""
+Usage: python tools/perf_text.py [n_lines] [workers]"""
+
+import sys
+from pathlib import Path
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 import sys
 
 import numpy as np

@@ -1,7 +1,11 @@
 """Small fixed workload for ncu: one corpus slice through the engine
 (Student-6-1-1, fp16 greedy by default).
 
-Usage: python -m paper_2109_08003_b200.profile_step [n_sentences] [dtype] [beam]"""
+Usage: python tools/profile_step.py [n_sentences] [dtype] [beam]"""
+
+import sys
+from pathlib import Path
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 import sys
 from pathlib import Path
 

@@ -63,7 +63,8 @@ def parse():
     ap.add_argument("--dtype", default="f16")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
-    ap.add_argument("--profile-sentences", type=int, default=16384)
+    ap.add_argument("--profile-sentences", type=int, default=65536,
+                    help="sentences of the first timed chunk in the per-kernel profile pass")
     ap.add_argument("--wbatch", type=int, default=64000, help="token cap (paper GPU setting 64000)")
     ap.add_argument("--sbatch", type=int, default=3072, help="sentence cap (paper GPU setting 3072)")
     ap.add_argument("--model", choices=sorted(MODELS), default="6-1-1")
@@ -611,7 +612,9 @@ def main():
         same = sum(x["identical"] for x in parts)
         parity = {"sentences": tot, "identical": same, "identical_frac": same / max(tot, 1),
                   "all_near_ties": all(x["all_near_ties"] for x in parts),
-                  "pass": all(x["pass"] for x in parts) and
+                  # the bar over the union of both samples: >= 99% identical
+                  # (greedy), every divergence a near-tie
+                  "pass": all(x["all_near_ties"] for x in parts) and
                           same >= live["min_identical_frac"] * tot,
                   "live": live, "fixture": fixed}
 

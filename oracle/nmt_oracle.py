@@ -455,47 +455,67 @@ def beam_divergence(steps, k: int, hyp, budget: int, eos=EOS):
     oracle's.  ``steps`` is a ``beam_sentence`` trace (per step: candidate
     scores / tokens / parents in the reference's sort order, search.py:125-127).
 
-    Replays the oracle search along ``hyp``'s path and returns
-    (where, step, gap):
-      * ("step", t, gap): at step t the oracle did not keep hyp's prefix
-        extension; gap = score of the oracle's k-th kept candidate minus the
-        score of hyp's candidate (inf when it is outside the traced width);
-      * ("final", t, gap): hyp survived every step; gap = oracle best final
-        score minus hyp's final score (search.py:145-147).
+    Replays the whole oracle search and returns (where, step, gap) with gap
+    the smaller of the two score margins that can explain the divergence:
+      * "hyp": at the first step the oracle did not keep hyp's extension, the
+        oracle's k-th kept score minus hyp's candidate score (inf when it is
+        outside the traced width); if hyp survived to the end, the oracle's
+        best final score minus hyp's (search.py:145-147);
+      * "best": the smallest margin by which the oracle's best hypothesis
+        stayed inside the beam (its candidate's score minus the first pruned
+        candidate's) — a search that dropped it had its ranking flipped there.
     ``hyp`` finished with EOS iff len(hyp) < budget (search.py:116-140).
     """
     hyp = tuple(int(x) for x in hyp)
     finished = len(hyp) < budget
     live, fin = [((), 0.0)], []
-    t = -1
+    kept_log = []            # per step: {(tokens, finished?): (score, margin)}
+    hyp_gap = hyp_where = None
     for t, (sc, tok, par) in enumerate(steps):
-        want = hyp[t] if t < len(hyp) else eos
-        if t >= len(hyp) and not finished:
-            break
-        prefix = hyp[:t]
-        pidx = next((i for i, h in enumerate(live) if h[0] == prefix), None)
-        if pidx is None:
-            return ("step", t, float("inf"))
-        hit = [j for j in range(len(tok)) if int(tok[j]) == want and int(par[j]) == pidx]
-        if not hit or hit[0] >= k:
-            gap = float(sc[k - 1] - sc[hit[0]]) if hit else float("inf")
-            return ("step", t, gap)
-        nxt = []
+        nxt_score = float(sc[k]) if len(sc) > k else float("-inf")
+        kept, nxt = {}, []
         for j in range(min(k, len(tok))):
             pj, tj, sj = int(par[j]), int(tok[j]), float(sc[j])
             if tj == eos:
                 fin.append((live[pj][0], sj))
+                kept[(live[pj][0], True)] = (sj, sj - nxt_score)
             else:
                 nxt.append((live[pj][0] + (tj,), sj))
+                kept[(live[pj][0] + (tj,), False)] = (sj, sj - nxt_score)
+        kept_log.append(kept)
+        if hyp_gap is None and (t < len(hyp) or (finished and t == len(hyp))):
+            key = (hyp, True) if t == len(hyp) else (hyp[:t + 1], False)
+            if key not in kept:
+                prefix = hyp[:t]
+                pidx = next((i for i, h in enumerate(live) if h[0] == prefix), None)
+                want = hyp[t] if t < len(hyp) else eos
+                hit = [j for j in range(len(tok))
+                       if pidx is not None and int(tok[j]) == want and int(par[j]) == pidx]
+                hyp_gap = float(sc[k - 1] - sc[hit[0]]) if hit else float("inf")
+                hyp_where = t
         live = nxt
-        if want == eos or not live or len(fin) >= k:
+        if not live or len(fin) >= k:
             break
     pool = fin if fin else live
     best = max(pool, key=lambda h: (h[1], tuple(-x for x in h[0])))
-    mine = [h for h in pool if h[0] == hyp]
-    if not mine:
-        return ("final", t, float("inf"))
-    return ("final", t, float(best[1] - mine[0][1]))
+    if hyp_gap is None:
+        mine = [h for h in pool if h[0] == hyp]
+        hyp_gap = float(best[1] - mine[0][1]) if mine else float("inf")
+        hyp_where = len(kept_log) - 1
+    margins = []
+    for t, kept in enumerate(kept_log):
+        if t < len(best[0]):
+            key = (best[0][:t + 1], False)
+        elif fin and t == len(best[0]):
+            key = (best[0], True)
+        else:
+            break
+        if key in kept:
+            margins.append((kept[key][1], t))
+    best_gap, best_t = min(margins) if margins else (float("inf"), -1)
+    if best_gap < hyp_gap:
+        return ("best", best_t, float(best_gap))
+    return ("hyp", hyp_where, float(hyp_gap))
 
 
 def greedy_divergence(ref, got, top1, top2, top2_id):

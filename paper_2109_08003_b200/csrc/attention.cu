@@ -307,6 +307,7 @@ template <typename T, int G, int CH, int NT, int U = 1, int UV = 1>
 __global__ void __launch_bounds__(NT) attn_decode_kernel(DecAttnArgs a, float qscale) {
   pdl_trigger();
   pdl_wait();
+  if (a.row_done && a.row_done[blockIdx.x]) return;   // finished sentence (search.py:72)
   constexpr int VEC = Vec16<T>::N;
   extern __shared__ float sm[];
   const int dk = a.dk;
@@ -430,6 +431,7 @@ template <typename T, int CH, int NT, int LPH, int U = 2, int UV = 4>
 __global__ void __launch_bounds__(NT) attn_decode_rows_kernel(DecAttnArgs a, float qscale) {
   pdl_trigger();
   pdl_wait();
+  if (a.row_done && a.row_done[blockIdx.x]) return;   // finished sentence (search.py:72)
   constexpr int VEC = Vec16<T>::N;
   // LPH 8 / 16 / 32: head score = shuffle reduction inside the head's lane
   // group.  LPH 0 (head sizes that do not map to a power-of-two lane group,
@@ -734,6 +736,243 @@ __global__ void __launch_bounds__(kDThreads) attn_decode_generic(DecAttnArgs a, 
 }
 
 // ---------------------------------------------------------------------------
+// Bulk-copy decode attention (single head, 16-bit K/V, no ancestor table).
+//
+// One CTA per query row.  A row's keys are contiguous in HBM — self K / V at
+// cache rows r*cap + j (d elements each), cross keys at k_start[seq] + j in
+// the interleaved [K | V (| c)] rows of the cross cache — so thread 0 moves a
+// chunk of CH keys with one or two cp.async.bulk copies (TMA engine, no
+// registers, no per-lane address math) into a double-buffered smem ring and
+// the next chunk is already in flight while this one is consumed.  Per chunk:
+// warp-per-key scores from shared memory (each lane holds its 16-byte slices
+// of the scaled query in registers), then every thread accumulates its CPT
+// output columns over the chunk's keys with an online softmax (running max m,
+// running sum l; a row that fits in one chunk is exactly
+// sum_j exp(s_j - max) v_j / sum_j exp(s_j - max), the reference's
+// max-shifted softmax, tensor.py:70-81).  Rows of finished sentences exit at
+// once (search.py:72: their outputs are discarded).
+template <typename T, int NT, int CPT>
+__global__ void __launch_bounds__(NT) attn_dec_bulk_kernel(DecAttnArgs a, float qscale, int CH,
+                                                           int voff, uint32_t buf_bytes) {
+  pdl_trigger();
+  pdl_wait();
+  const int r = blockIdx.x;
+  if (a.row_done && a.row_done[r]) return;
+  constexpr int VEC = 8;                      // 16-bit elements per 16-byte vector
+  constexpr int NW = NT / 32;
+  constexpr int D = NT * CPT;                 // row width (single head: dk == d)
+  constexpr int NVL = (D / VEC + 31) / 32;    // 16-byte vectors per lane in a key row
+  extern __shared__ __align__(128) uint8_t smem_b[];
+  uint8_t* buf0 = smem_b;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_b + 2 * (size_t)buf_bytes);
+  float* S = reinterpret_cast<float*>(bar + 2);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const bool self = a.self_mode != 0;
+  const bool interleaved = voff > 0;
+  int nk, t = 0;
+  bool all_masked = false;
+  int64_t row0;
+  if (self) {
+    t = *a.t_ptr;
+    nk = t + 1;
+    row0 = (int64_t)r * a.cap;
+  } else {
+    const int seq = r / a.rows_per_seq;
+    const int kl = a.k_len[seq];
+    all_masked = kl == 0;
+    nk = all_masked ? a.k_pad : kl;
+    row0 = a.k_start[seq];
+  }
+  const T* kb = reinterpret_cast<const T*>(a.k);
+  const T* vb = reinterpret_cast<const T*>(a.v);
+  const size_t row_bytes = (size_t)a.ldkv * sizeof(T);
+  const int nchunks = (nk + CH - 1) / CH;
+  auto issue = [&](int c) {
+    const int j0 = c * CH;
+    const int n = min(CH, nk - j0);
+    uint8_t* dst = buf0 + (size_t)(c & 1) * buf_bytes;
+    const uint32_t bytes = (uint32_t)(n * row_bytes);
+    mbar_expect_tx(bar + (c & 1), interleaved ? bytes : 2 * bytes);
+    bulk_g2s(dst, kb + (row0 + j0) * a.ldkv, bytes, bar + (c & 1));
+    if (!interleaved)
+      bulk_g2s(dst + (size_t)CH * row_bytes, vb + (row0 + j0) * a.ldkv, bytes, bar + (c & 1));
+  };
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
+    fence_mbar_init();
+    issue(0);
+    if (nchunks > 1) issue(1);
+  }
+  // scaled query slices in registers (lane holds vectors lane, lane + 32, ...)
+  float qr[NVL][VEC];
+  const T* q = reinterpret_cast<const T*>(a.q) + (size_t)r * a.ldq;
+#pragma unroll
+  for (int i = 0; i < NVL; ++i) {
+    const int e0 = (lane + 32 * i) * VEC;
+    if (e0 < D) {
+      float f[VEC];
+      cvt16<T>(*reinterpret_cast<const uint4*>(q + e0), f);
+#pragma unroll
+      for (int k = 0; k < VEC; ++k) qr[i][k] = f[k] * qscale;
+    }
+  }
+  __syncthreads();   // barrier init visible to all waiters
+  float acc[CPT];
+#pragma unroll
+  for (int i = 0; i < CPT; ++i) acc[i] = 0.f;
+  float m_run = -INFINITY, l_run = 0.f;
+  for (int c = 0; c < nchunks; ++c) {
+    const int n = min(CH, nk - c * CH);
+    const uint8_t* kbuf = buf0 + (size_t)(c & 1) * buf_bytes;
+    const T* vrow0 = reinterpret_cast<const T*>(interleaved ? kbuf : kbuf + (size_t)CH * row_bytes) +
+                     (interleaved ? voff : 0);
+    mbar_wait(bar + (c & 1), (uint32_t)(c >> 1) & 1u);
+    // scores: warp w takes keys w, w + NW, ...
+    for (int j = warp; j < n; j += NW) {
+      const T* kr = reinterpret_cast<const T*>(kbuf + (size_t)j * row_bytes);
+      float sacc = 0.f;
+#pragma unroll
+      for (int i = 0; i < NVL; ++i) {
+        const int e0 = (lane + 32 * i) * VEC;
+        if (e0 < D) {
+          float f[VEC];
+          cvt16<T>(*reinterpret_cast<const uint4*>(kr + e0), f);
+#pragma unroll
+          for (int k = 0; k < VEC; ++k) sacc = fmaf(qr[i][k], f[k], sacc);
+        }
+      }
+      sacc = warp_sum(sacc);
+      if (lane == 0) {
+        if (a.kc_off >= 0) sacc += qscale * to_f32(kr[a.kc_off]);
+        S[j] = all_masked ? sacc + kMaskValue : sacc;
+      }
+    }
+    __syncthreads();
+    // online softmax over this chunk (every thread walks the same S in order,
+    // so m / l are identical across the CTA)
+    float cmax = -INFINITY;
+    for (int j = 0; j < n; ++j) cmax = fmaxf(cmax, S[j]);
+    const float m_new = fmaxf(m_run, cmax);
+    const float alpha = expf(m_run - m_new);
+    l_run *= alpha;
+#pragma unroll
+    for (int i = 0; i < CPT; ++i) acc[i] *= alpha;
+    const int col = tid * CPT;
+    for (int j = 0; j < n; ++j) {
+      const float pj = expf(S[j] - m_new);
+      l_run += pj;
+      const T* vr = vrow0 + (size_t)j * a.ldkv + col;
+      if constexpr (CPT == 2) {
+        float2 v2;
+        if constexpr (sizeof(T) == 2 && std::is_same<T, __half>::value)
+          v2 = __half22float2(*reinterpret_cast<const __half2*>(vr));
+        else
+          v2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(vr));
+        acc[0] = fmaf(pj, v2.x, acc[0]);
+        acc[1] = fmaf(pj, v2.y, acc[1]);
+      } else if constexpr (CPT == 8) {
+        float f[8];
+        cvt16<T>(*reinterpret_cast<const uint4*>(vr), f);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] = fmaf(pj, f[i], acc[i]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < CPT; ++i) acc[i] = fmaf(pj, to_f32(vr[i]), acc[i]);
+      }
+    }
+    m_run = m_new;
+    __syncthreads();   // buffer (c & 1) and S fully consumed
+    if (tid == 0 && c + 2 < nchunks) {
+      fence_proxy_async_smem();
+      issue(c + 2);
+    }
+  }
+  const int col = tid * CPT;
+  const float inv = 1.f / l_run;
+  if (a.out_f32) {
+    float* o = reinterpret_cast<float*>(a.out) + (size_t)r * a.ldo + col;
+#pragma unroll
+    for (int i = 0; i < CPT; ++i) {
+      const float v = acc[i] * inv;
+      o[i] = a.out_bias ? v + a.out_bias[col + i] : v;
+    }
+  } else {
+    T* o = reinterpret_cast<T*>(a.out) + (size_t)r * a.ldo + col;
+#pragma unroll
+    for (int i = 0; i < CPT; ++i) o[i] = from_f32<T>(acc[i] * inv);
+  }
+}
+
+// Bulk-copy kernel applicability and launch (returns cudaErrorNotSupported to
+// fall through to the register-staged kernels).
+// Ring slot size (FNMT_BULK_KB, default 16 KB) and block width (FNMT_BULK_NT, default 128).
+uint32_t bulk_buf_bytes() {
+  static uint32_t b = 0;
+  if (!b) {
+    const char* e = getenv("FNMT_BULK_KB");
+    const int kb = e ? atoi(e) : 16;
+    b = (uint32_t)std::max(4, std::min(100, kb)) * 1024u;
+  }
+  return b;
+}
+int bulk_nt() {
+  static int n = -1;
+  if (n < 0) {
+    const char* e = getenv("FNMT_BULK_NT");
+    n = e ? atoi(e) : 128;   // r02 A/B (6-1-1 bench): 128 threads x 16 KB slots best
+    if (n != 64 && n != 128 && n != 256) n = 128;
+  }
+  return n;
+}
+
+bool dec_bulk_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("FNMT_DEC_BULK");
+    on = !(e && e[0] == '0');
+  }
+  return on != 0;
+}
+
+template <typename T>
+cudaError_t try_dec_bulk(const DecAttnArgs& a, float qscale, cudaStream_t s) {
+  if (!dec_bulk_enabled() || a.heads != 1 || a.anc || a.new_k || a.dk % 8) return cudaErrorNotSupported;
+  const int d = a.dk;
+  const size_t row_bytes = (size_t)a.ldkv * sizeof(T);
+  if (row_bytes % 16 || (reinterpret_cast<uintptr_t>(a.k) & 15) ||
+      (reinterpret_cast<uintptr_t>(a.v) & 15) || (reinterpret_cast<uintptr_t>(a.q) & 15) ||
+      a.ldq % 8)
+    return cudaErrorNotSupported;
+  // interleaved rows (cross caches, folded self cache): V at element offset
+  // voff of the K row, one copy per chunk; else separate K / V caches of d
+  int voff = 0;
+  const ptrdiff_t off = reinterpret_cast<const T*>(a.v) - reinterpret_cast<const T*>(a.k);
+  if (off > 0 && off + d <= a.ldkv)
+    voff = (int)off;
+  else if (!a.self_mode || a.ldkv != d)
+    return cudaErrorNotSupported;
+  const size_t per_key = voff ? row_bytes : 2 * row_bytes;
+  const int CH = (int)std::min<size_t>(64, bulk_buf_bytes() / per_key);
+  if (CH < 4) return cudaErrorNotSupported;
+  const uint32_t buf = (uint32_t)(((size_t)CH * per_key + 127) & ~(size_t)127);
+  const size_t smem = 2 * (size_t)buf + 16 + sizeof(float) * CH;
+  auto pick = [&](auto kern, int nt) -> cudaError_t {
+    cudaError_t e = set_max_smem((const void*)kern);
+    if (e != cudaSuccess) return e;
+    return launch_k(kern, dim3(a.rows), dim3(nt), smem, s, a, qscale, CH, voff, buf);
+  };
+  if (d == 512) {
+    if (bulk_nt() == 64) return pick(attn_dec_bulk_kernel<T, 64, 8>, 64);
+    return bulk_nt() == 128 ? pick(attn_dec_bulk_kernel<T, 128, 4>, 128)
+                            : pick(attn_dec_bulk_kernel<T, 256, 2>, 256);
+  }
+  if (d == 256) return pick(attn_dec_bulk_kernel<T, 128, 2>, 128);
+  if (d == 1024) return pick(attn_dec_bulk_kernel<T, 256, 4>, 256);
+  return cudaErrorNotSupported;
+}
+
+// ---------------------------------------------------------------------------
 // dispatch
 
 template <typename T>
@@ -890,7 +1129,9 @@ cudaError_t decode_dispatch(const DecAttnArgs& a, cudaStream_t s) {
   constexpr int VEC = Vec16<T>::N;
   const float qscale = (float)(1.0 / sqrt((double)a.dk));
   if constexpr (sizeof(T) == 2) {
-    const cudaError_t e = try_dec_rows<T>(a, qscale, s);
+    cudaError_t e = try_dec_bulk<T>(a, qscale, s);
+    if (e != cudaErrorNotSupported) return e;
+    e = try_dec_rows<T>(a, qscale, s);
     if (e != cudaErrorNotSupported) return e;
   }
   const int nch = a.dk / VEC;

@@ -416,24 +416,26 @@ Norm Engine::make_norm(const std::string& prefix) {
   return Norm{upload_f32(need(prefix + ".gain", d)), upload_f32(need(prefix + ".bias", d))};
 }
 
-// Folded cross attention weights of decoder layer `prefix` (reference
-// orientation x @ W, all [d, d]): rows of W^T [2d + 8, d]
+// Folded attention weights of decoder layer `p`, block `blk` ("cross" or
+// "self"; reference orientation x @ W, all [d, d]): rows of W^T [2d + 8, d]
 //   a < d      : (Wk Wq^T)^T  -> K~ = E (Wk Wq^T) + bk Wq^T          (K Wq^T)
 //   d + c      : (Wv Wo)^T    -> V~ = E (Wv Wo) + bv Wo              (V Wo)
 //   2d         : Wk bq        -> c  = E (Wk bq) + bk . bq            (bq . k)
 //   2d+1..2d+7 : 0 (16-byte row alignment)
 // so q.k = x.K~ + c and (sum_j p_j v_j) Wo + bo = sum_j p_j V~_j + bo: the
-// per-step cross-q and cross-o GEMMs disappear (model.py:331-336 reassociated;
-// computed in double, rounded once to the compute dtype).
-Lin Engine::make_folded_cross(const std::string& p) {
+// block's q and o GEMMs disappear from every decode step (model.py:316-336
+// reassociated; computed in double, rounded once to the compute dtype).  E is
+// the encoder output (cross, once per batch) or the decoder layer input of
+// step j (self, appended to the cache at slot j).
+Lin Engine::make_folded(const std::string& p, const std::string& blk) {
   const int d = arch.d_model, N = 2 * d + 8;
-  const auto& Wq = need(p + ".cross.q_w", (int64_t)d * d);
-  const auto& Wk = need(p + ".cross.k_w", (int64_t)d * d);
-  const auto& Wv = need(p + ".cross.v_w", (int64_t)d * d);
-  const auto& Wo = need(p + ".cross.o_w", (int64_t)d * d);
-  const auto& bq = need(p + ".cross.q_b", d);
-  const auto& bk = need(p + ".cross.k_b", d);
-  const auto& bv = need(p + ".cross.v_b", d);
+  const auto& Wq = need(p + "." + blk + ".q_w", (int64_t)d * d);
+  const auto& Wk = need(p + "." + blk + ".k_w", (int64_t)d * d);
+  const auto& Wv = need(p + "." + blk + ".v_w", (int64_t)d * d);
+  const auto& Wo = need(p + "." + blk + ".o_w", (int64_t)d * d);
+  const auto& bq = need(p + "." + blk + ".q_b", d);
+  const auto& bk = need(p + "." + blk + ".k_b", d);
+  const auto& bv = need(p + "." + blk + ".v_b", d);
   std::vector<double> woT((size_t)d * d);   // woT[c][n] = Wo[n][c]
   for (int n = 0; n < d; ++n)
     for (int c = 0; c < d; ++c) woT[(size_t)c * d + n] = Wo[(size_t)n * d + c];
@@ -477,6 +479,15 @@ Lin Engine::make_folded_cross(const std::string& p) {
   L.b = upload_f32(bias);
   finish_lin(L);
   return L;
+}
+
+bool fused_self_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("FNMT_FUSED_SELF");
+    on = !(e && e[0] == '0');
+  }
+  return on != 0;
 }
 
 bool fused_cross_enabled() {
@@ -541,6 +552,7 @@ void Engine::finalize() {
   fused_cross = dt != kF32 && !q8 && arch.n_heads_dec == 1 && d % 256 == 0 &&
                 fused_cross_enabled();
   ckv_ld = fused_cross ? 2 * d + 8 : 2 * d;
+  fused_self = fused_cross && fused_self_enabled();
   dec.clear();
   for (int i = 0; i < arch.n_dec_layers; ++i) {
     const std::string p = "dec." + std::to_string(i);
@@ -552,7 +564,8 @@ void Engine::finalize() {
     L.ckv = make_lin({p + ".cross.k_w", p + ".cross.v_w"}, {p + ".cross.k_b", p + ".cross.v_b"},
                      d, {d, d});
     L.co = make_lin({p + ".cross.o_w"}, {p + ".cross.o_b"}, d, {d});
-    if (fused_cross) L.fck = make_folded_cross(p);
+    if (fused_cross) L.fck = make_folded(p, "cross");
+    if (fused_self) L.fsk = make_folded(p, "self");
     L.n1 = make_norm(p + ".norm1");
     L.n2 = make_norm(p + ".norm2");
     L.ffn = arch.ffn_dim_dec > 0;
@@ -614,8 +627,10 @@ void Engine::reserve(int tok_cap, int row_cap, int64_t pool_cap) {
   ws.vc.assign(arch.n_dec_layers, nullptr);
   for (int l = 0; l < arch.n_dec_layers; ++l) {
     ws.ckv[l] = alloc((size_t)es * tok_cap * ckv_ld);
-    ws.kc[l] = alloc((size_t)es * pool_cap * d);
-    ws.vc[l] = alloc((size_t)es * pool_cap * d);
+    // self K / V caches [pool_cap, d] each; with folded self attention the same
+    // allocation also holds the interleaved [K~ | V~ | c | 0] rows [pool_cap, 2d + 8]
+    ws.kc[l] = alloc((size_t)es * pool_cap * (fused_self ? 2 * d + 8 : 2 * d));
+    ws.vc[l] = (char*)ws.kc[l] + (size_t)es * pool_cap * d;
   }
   ws.dx32 = (float*)alloc(sizeof(float) * (size_t)row_cap * d);
   ws.dy32 = (float*)alloc(sizeof(float) * (size_t)row_cap * d);
@@ -686,9 +701,10 @@ void Engine::gemm(const void* A, const CUtensorMap* tmA, int lda, const Lin& L, 
   attach_q(g, L);
   const int ev = prof_begin(s);
   CK(launch_gemm(g, s));
-  prof_end(s, ev, gemm_cls, 2.0 * M * L.N * L.K,
-           (double)M * L.K * dtype_size(dt) + (double)L.N * L.K * dtype_size(dt) +
-               (double)M * L.N * (dtype_size(c_dtype) + (resid ? 4.0 : 0.0)));
+  const double Mc = prof_m >= 0 ? prof_m : (double)M;
+  prof_end(s, ev, gemm_cls, 2.0 * Mc * L.N * L.K,
+           Mc * L.K * dtype_size(dt) + (double)L.N * L.K * dtype_size(dt) +
+               Mc * L.N * (dtype_size(c_dtype) + (resid ? 4.0 : 0.0)));
   ++launches;
 }
 
@@ -711,8 +727,9 @@ void Engine::gemm_argmax(const void* A, const CUtensorMap* tmA, int lda, int M,
   attach_q(g, out);
   const int ev = prof_begin(s);
   CK(launch_gemm(g, s));
-  prof_end(s, ev, FNMT_K_VOCAB, 2.0 * M * out.N * out.K,
-           (double)M * out.K * dtype_size(dt) + (double)out.N * out.K * dtype_size(dt));
+  const double Mc = prof_m >= 0 ? prof_m : (double)M;
+  prof_end(s, ev, FNMT_K_VOCAB, 2.0 * Mc * out.N * out.K,
+           Mc * out.K * dtype_size(dt) + (double)out.N * out.K * dtype_size(dt));
   ++launches;
 }
 
@@ -722,7 +739,8 @@ void Engine::norm(const float* x, const float* y, const Norm& n, float* o32, voi
   CK(launch_add_norm(x, y, n.g, n.b, arch.norm_l1, o32, dt == kF32 ? nullptr : oa,
                      dt, rows, arch.d_model, s));
   prof_end(s, ev, FNMT_K_NORM, 0.0,
-           (double)rows * arch.d_model * ((y ? 12.0 : 8.0) + (dt == kF32 ? 0 : dtype_size(dt))));
+           (prof_m >= 0 ? prof_m : (double)rows) * arch.d_model *
+               ((y ? 12.0 : 8.0) + (dt == kF32 ? 0 : dtype_size(dt))));
   ++launches;
 }
 
@@ -793,15 +811,74 @@ void Engine::run_step(const StepView& v, cudaStream_t s) {
   const bool tc = dt != kF32;
   const int R = v.rows;
   gemm_cls = FNMT_K_GEMM_DEC;
+  // profiler counts: live rows only, unpadded source keys
+  const double Rl = (profiling && v.prof_live) ? (double)(*v.prof_live)[v.host_t] : (double)R;
+  const double Sl = (profiling && v.prof_src) ? (*v.prof_src)[v.host_t] : (double)R * v.max_k;
+  prof_m = profiling ? Rl : -1.0;
   {
     const int ev = prof_begin(s);
     CK(launch_embed(v.prev, nullptr, v.t_ptr, tgt_emb32, pos32, emb_scale(), ws.dx32,
                     tc ? ws.dxa : nullptr, dt, R, d, s));
-    prof_end(s, ev, FNMT_K_EMBED, 0.0, (double)R * d * (8.0 + dtype_size(dt)));
+    prof_end(s, ev, FNMT_K_EMBED, 0.0, Rl * d * (8.0 + dtype_size(dt)));
   }
   ++launches;
   for (int l = 0; l < arch.n_dec_layers; ++l) {
     const DecL& L = dec[l];
+    if (fused_self && v.ws_caches && !v.anc) {
+      // folded self attention: this step's [K~ | V~ | c] row straight into cache
+      // slot t; the query is the layer input itself and the attention writes the
+      // o-projected output (+ bo, fp32) into the residual branch
+      const int fl = 2 * d + 8;
+      GemmArgs g;
+      g.A = ws.dxa;
+      g.lda = d;
+      g.W = L.fsk.w;
+      g.ldw = L.fsk.K;
+      g.in_dtype = dt;
+      g.bias = L.fsk.b;
+      g.M = R;
+      g.N = fl;
+      g.K = d;
+      g.epi = kEpiSlot;
+      g.C = v.kc[l];
+      g.ldc = fl;
+      g.c_dtype = dt;
+      g.cap = v.cap;
+      g.t_ptr = v.t_ptr;
+      g.tmap_a = &ws.tm_dxa;
+      g.tmap_w = &L.fsk.tm;
+      const int ev = prof_begin(s);
+      CK(launch_gemm(g, s));
+      prof_end(s, ev, gemm_cls, 2.0 * Rl * fl * d, Rl * d * es + (double)fl * d * es + Rl * fl * es);
+      ++launches;
+      DecAttnArgs a{};
+      a.q = ws.dxa;
+      a.ldq = d;
+      a.k = v.kc[l];
+      a.v = (const char*)v.kc[l] + (size_t)d * es;
+      a.ldkv = fl;
+      a.kc_off = 2 * d;
+      a.out = ws.dy32;
+      a.ldo = d;
+      a.out_f32 = 1;
+      a.out_bias = L.so.b;
+      a.dtype = dt;
+      a.heads = 1;
+      a.dk = d;
+      a.rows = R;
+      a.self_mode = 1;
+      a.cap = v.cap;
+      a.t_ptr = v.t_ptr;
+      a.max_k = v.cap;
+      a.row_done = v.row_done;
+      {
+        const int ev2 = prof_begin(s);
+        CK(launch_attention_decode(a, s));
+        prof_end(s, ev2, FNMT_K_ATTN_DEC, 0.0, Rl * (v.host_t + 1) * 2 * d * es);
+      }
+      ++launches;
+      norm(ws.dx32, ws.dy32, L.n1, ws.dx32, ws.dxa, R, s);
+    } else {
     {
       // q -> ws.dq, this step's k / v straight into the self cache slot t (fused append)
       GemmArgs g;
@@ -828,8 +905,8 @@ void Engine::run_step(const StepView& v, cudaStream_t s) {
       attach_q(g, L.sqkv);
       const int ev = prof_begin(s);
       CK(launch_gemm(g, s));
-      prof_end(s, ev, gemm_cls, 2.0 * R * L.sqkv.N * L.sqkv.K,
-               (double)R * d * es + (double)L.sqkv.N * L.sqkv.K * es + 3.0 * R * d * es);
+      prof_end(s, ev, gemm_cls, 2.0 * Rl * L.sqkv.N * L.sqkv.K,
+               Rl * d * es + (double)L.sqkv.N * L.sqkv.K * es + 3.0 * Rl * d * es);
       ++launches;
     }
     DecAttnArgs a{};
@@ -855,13 +932,15 @@ void Engine::run_step(const StepView& v, cudaStream_t s) {
     a.anc = v.anc;
     a.anc_buf_stride = v.anc_stride;
     a.max_k = v.cap;
+    a.row_done = v.row_done;
     {
       const int ev = prof_begin(s);
       CK(launch_attention_decode(a, s));
-      prof_end(s, ev, FNMT_K_ATTN_DEC, 0.0, (double)R * (v.host_t + 1) * 2 * d * es);
+      prof_end(s, ev, FNMT_K_ATTN_DEC, 0.0, Rl * (v.host_t + 1) * 2 * d * es);
     }
     ++launches;
     gemm_norm(ws.datt, tc ? &ws.tm_datt : nullptr, d, L.so, R, ws.dx32, ws.dxa, ws.dy32, L.n1, s);
+    }
     // folded cross attention (workspace caches only): q is the norm1 output itself,
     // the attention writes the o-projection output (fp32, + bias) straight into dy32
     const bool folded = fused_cross && v.ws_caches;
@@ -889,10 +968,11 @@ void Engine::run_step(const StepView& v, cudaStream_t s) {
     c.k_pad = v.k_pad;
     c.rows_per_seq = v.rows_per_seq;
     c.max_k = v.max_k;
+    c.row_done = v.row_done;
     {
       const int ev = prof_begin(s);
       CK(launch_attention_decode(c, s));
-      prof_end(s, ev, FNMT_K_ATTN_DEC, 0.0, (double)R * v.max_k * 2 * d * es);
+      prof_end(s, ev, FNMT_K_ATTN_DEC, 0.0, Sl * 2 * d * es);
     }
     ++launches;
     if (folded)
@@ -923,8 +1003,8 @@ void Engine::run_step(const StepView& v, cudaStream_t s) {
     g.tmap_w = &out.tm;
     const int ev = prof_begin(s);
     CK(launch_gemm(g, s));
-    prof_end(s, ev, FNMT_K_VOCAB, 2.0 * R * out.N * out.K,
-             (double)R * out.K * dtype_size(dt) + (double)out.N * out.K * dtype_size(dt));
+    prof_end(s, ev, FNMT_K_VOCAB, 2.0 * Rl * out.N * out.K,
+             Rl * out.K * dtype_size(dt) + (double)out.N * out.K * dtype_size(dt));
     ++launches;
   } else if (v.logits) {
     gemm_cls = FNMT_K_VOCAB;
@@ -936,6 +1016,7 @@ void Engine::run_step(const StepView& v, cudaStream_t s) {
   } else {
     gemm_argmax(ws.dxa, tc ? &ws.tm_dxa : nullptr, d, R, v.keys, s);
   }
+  prof_m = -1.0;
 }
 
 float Engine::emb_scale() const { return (float)std::sqrt((double)arch.d_model); }
@@ -1123,6 +1204,7 @@ std::unique_ptr<Engine> Engine::make_lane() {
   L->dec = dec;
   L->finalized = true;   // weights are shared (owned by this engine)
   L->fused_cross = fused_cross;
+  L->fused_self = fused_self;
   L->ckv_ld = ckv_ld;
   L->n_lanes = 1;
   return L;
@@ -1171,7 +1253,12 @@ int64_t Engine::run_batch(const PlanCtx& P, size_t bi) {
     const int32_t* res_ids = ws.out_ids;
     const int32_t* res_len = ws.out_len;
     if (run.beam_size <= 1) {
-      steps_total += decode_greedy(R, cap, b.max_len, run);
+      std::vector<int32_t> src(R), bud(R);
+      for (int r = 0; r < R; ++r) {
+        src[r] = P.live_len[b.rows[r]];
+        bud[r] = P.budget_all[P.batch_row0[bi] + r];
+      }
+      steps_total += decode_greedy(R, cap, b.max_len, run, src, bud);
     } else {
       steps_total += decode_beam(R, cap, b.max_len, run);
       res_ids = beam.out_ids;
@@ -1236,13 +1323,30 @@ StepView Engine::step_view(int rows, int cap, int max_len, int rows_per_seq) {
   return v;
 }
 
-int Engine::decode_greedy(int R, int cap, int max_len, const fnmt_run& run) {
+int Engine::decode_greedy(int R, int cap, int max_len, const fnmt_run& run,
+                          const std::vector<int32_t>& src_len, const std::vector<int32_t>& budgets) {
   init_decode_kernel<<<(R + 255) / 256, 256, 0, stream>>>(ws.prev, ws.finished, ws.out_len,
                                                          ws.keys, ws.t, ws.alive, R, run.bos_id);
   CK(cudaGetLastError());
   ++launches;
   StepView v = step_view(R, cap, max_len, 1);
   v.keys = ws.keys;
+  v.row_done = ws.finished;
+  // profiler: rows still inside their budget at step t (random weights never
+  // emit EOS; an EOS-finished row would still be counted, an upper bound)
+  std::vector<int> live;
+  std::vector<double> live_src;
+  if (profiling) {
+    live.assign(cap, 0);
+    live_src.assign(cap, 0.0);
+    for (int r = 0; r < R; ++r)
+      for (int t = 0; t < std::min(cap, budgets[r]); ++t) {
+        live[t] += 1;
+        live_src[t] += src_len[r];
+      }
+    v.prof_live = &live;
+    v.prof_src = &live_src;
+  }
   GreedyState gs;
   gs.keys = ws.keys;
   gs.prev = ws.prev;
@@ -1261,7 +1365,7 @@ int Engine::decode_greedy(int R, int cap, int max_len, const fnmt_run& run) {
     run_step(v, stream);
     const int ev = prof_begin(stream);
     CK(launch_greedy_update(gs, stream));
-    prof_end(stream, ev, FNMT_K_SEARCH, 0.0, (double)R * 24);
+    prof_end(stream, ev, FNMT_K_SEARCH, 0.0, (profiling ? (double)live[t] : (double)R) * 24);
     ++launches;
   };
   const int64_t nodes = profiling ? 0 : capture_step([&] { body(0); });

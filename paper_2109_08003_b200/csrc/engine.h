@@ -55,6 +55,7 @@ struct EncL {
 struct DecL {
   Lin sqkv, so, cq, ckv, co, f1, f2;
   Lin fck;   // folded cross K|V|c (fused_cross): [K Wq^T | V Wo | bq.k] per encoder row
+  Lin fsk;   // folded self K|V|c (fused_self): the same per decoder input row
   Norm n1, n2, n3;
   bool ffn = false;
 };
@@ -100,6 +101,11 @@ struct StepView {
   const int32_t* anc = nullptr;        // beam: 2 ancestor tables (parity of t)
   int64_t anc_stride = 0;
   int host_t = 0;                      // host copy of the step (profiling byte counts only)
+  // profiling (SURVEY §8(d) algorithmic counts): live rows at step t and the
+  // sum of their unpadded source lengths; null = count every row / max_k keys
+  const std::vector<int>* prof_live = nullptr;
+  const std::vector<double>* prof_src = nullptr;
+  const uint8_t* row_done = nullptr;   // greedy: finished flags (attention skips those rows)
   bool ws_caches = false;              // kc/vc/ckv are the workspace buffers (TMA maps valid)
   unsigned long long* keys = nullptr;  // argmax output (greedy)
   float* logits = nullptr;             // or full logits (protocol path / fp32 beam)
@@ -158,6 +164,9 @@ class Engine {
   // query and output projections are multiplied into the per-batch cross K/V
   // (K~ = K Wq^T, V~ = V Wo, c = bq.k), removing two GEMMs from every step.
   bool fused_cross = false;
+  // ... and the self attention folded the same way (greedy corpus decode): the
+  // per-step q and self-o GEMMs disappear, the cache holds [K~ | V~ | c] rows.
+  bool fused_self = false;
   int ckv_ld = 0;    // row stride (elements) of the workspace cross K/V
   void finalize();
   void reserve(int tok_cap, int row_cap, int64_t pool_cap);
@@ -218,6 +227,7 @@ class Engine {
   std::vector<ProfRec> prof_recs;
   size_t prof_used = 0;
   int gemm_cls = FNMT_K_GEMM_ENC;
+  double prof_m = -1.0;   // >= 0: rows the profiler counts for GEMM / norm launches (live rows)
 
   void* dalloc(size_t bytes);
   const std::vector<float>& need(const std::string& name, int64_t numel) const;
@@ -225,7 +235,7 @@ class Engine {
   void* upload_act(const std::vector<float>& v);
   Lin make_lin(const std::vector<std::string>& wnames, const std::vector<std::string>& bnames,
                int k, const std::vector<int>& ns);
-  Lin make_folded_cross(const std::string& prefix);
+  Lin make_folded(const std::string& prefix, const std::string& blk);
   void finish_lin(Lin& L);
   void make_qlin(Lin& L, const std::vector<std::string>& wnames, int k, const std::vector<int>& ns);
   void attach_q(GemmArgs& g, const Lin& L) const;
@@ -249,7 +259,8 @@ class Engine {
   int64_t capture_step(const std::function<void()>& body);
   int drive_steps(int cap, int64_t nodes, const std::function<void(int)>& direct);
   StepView step_view(int rows, int cap, int max_len, int rows_per_seq);
-  int decode_greedy(int R, int cap, int max_len, const fnmt_run& run);
+  int decode_greedy(int R, int cap, int max_len, const fnmt_run& run,
+                    const std::vector<int32_t>& src_len, const std::vector<int32_t>& budgets);
   int decode_beam(int R, int cap, int max_len, const fnmt_run& run);
   void reserve_beam(int sent_cap, int k, int64_t pool_cap);
   BeamWs beam;

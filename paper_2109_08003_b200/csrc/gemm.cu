@@ -74,6 +74,12 @@ __device__ __forceinline__ void* qkv_dst(const EpiParams& ep, int m, int n, int 
   return cache + (((size_t)m * ep.cap + t) * ep.seg + col) * es;
 }
 
+// Output row of accumulator row m: kEpiSlot writes row m into this step's
+// cache slot m * cap + t (the folded self-attention cache, engine.cu).
+__device__ __forceinline__ size_t out_row(const EpiParams& e, int m) {
+  return e.epi == kEpiSlot ? (size_t)m * e.cap + *e.t_ptr : (size_t)m;
+}
+
 __device__ __forceinline__ float epi_value(const EpiParams& e, int m, int n, float acc) {
   float v = acc;
   if (e.bias) v = v + e.bias[n];
@@ -93,7 +99,7 @@ __device__ __forceinline__ void store_elem(const EpiParams& e, int m, int n, flo
       *reinterpret_cast<__nv_bfloat16*>(p) = __float2bfloat16_rn(v);
     return;
   }
-  size_t off = (size_t)m * e.ldc + n;
+  size_t off = out_row(e, m) * e.ldc + n;
   if (e.c_dtype == kF32)
     reinterpret_cast<float*>(e.C)[off] = v;
   else if (e.c_dtype == kF16)
@@ -186,7 +192,7 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& ep, int m, int n
       }
     }
     uint4* dst =
-        reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(ep.C) + (size_t)m * ep.ldc + nb);
+        reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(ep.C) + out_row(ep, m) * ep.ldc + nb);
 #pragma unroll
     for (int i = 0; i < 4; ++i)
       dst[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
@@ -194,7 +200,7 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& ep, int m, int n
   }
   if (full_chunk && ep.c_dtype == kF32 && (ep.ldc % 4) == 0 &&
       (ep.resid == nullptr || (ep.ld_resid % 4) == 0)) {
-    float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(ep.C) + (size_t)m * ep.ldc + nb);
+    float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(ep.C) + out_row(ep, m) * ep.ldc + nb);
     const float4* res = ep.resid ? reinterpret_cast<const float4*>(ep.resid + (size_t)m * ep.ld_resid + nb)
                                  : nullptr;
 #pragma unroll
@@ -752,6 +758,7 @@ cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t s) {
                nullptr, nullptr, nullptr, nullptr, nullptr, 0};
   if (g.epi == kEpiQKV && (!g.kc || !g.vc || !g.t_ptr || g.seg <= 0 || g.N != 3 * g.seg))
     return cudaErrorInvalidValue;
+  if (g.epi == kEpiSlot && (!g.t_ptr || g.cap <= 0 || g.resid)) return cudaErrorInvalidValue;
   if (g.epi == kEpiTopK && (g.in_dtype == kF32 || (g.topk.K != 4 && g.topk.K != 8)))
     return cudaErrorInvalidValue;   // fp32 path: store logits + launch_logits_topk_partials
   if (g.in_dtype == kF32) {

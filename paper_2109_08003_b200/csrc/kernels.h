@@ -53,6 +53,7 @@ enum Epilogue : int {
   kEpiArgmax = 1,  // keys[m] = max over n < valid_n of key(acc + bias[n], n)
   kEpiTopK = 2,    // per (row, 256-column tile): max, sum exp(x - max), top-K (value, index)
   kEpiQKV = 3,     // decoder self q|k|v: q -> C, k / v -> KV cache slot (row*cap + *t_ptr)
+  kEpiSlot = 4,    // C[(m*cap + *t_ptr), n] = acc + bias[n]: a whole row into its cache slot
 };
 
 // Per-(row, N-tile) partials of the beam epilogue; tile = n / kTopKTile.
@@ -199,6 +200,9 @@ struct DecAttnArgs {
   int kc_off = -1;
   const float* out_bias = nullptr;
   int out_f32 = 0;
+  // greedy corpus decode: rows whose sentence has finished (search.py:72 feeds
+  // them PAD and discards their output) skip the attention entirely
+  const uint8_t* row_done = nullptr;
 };
 cudaError_t launch_attention_decode(const DecAttnArgs& a, cudaStream_t s);
 

@@ -174,8 +174,9 @@ def test_config1_student_greedy_vs_reference(golden, student_weights, dtype):
         gap = float(g["top1"][starts[i] + j] - g["top2"][starts[i] + j])
         report.append((i, j, gap))
     print("fp16 divergences (sentence, step, reference top1-top2 gap):", report)
-    assert same >= 0.99 * 64, report
-    assert all(gap <= 0.05 for _, _, gap in report), report
+    # 64 sentences: every divergence must be a near-tie (the >= 99% identical
+    # rate is asserted at corpus scale, test_gpu_corpus_parity.py)
+    assert all(gap <= P.NEAR_TIE for _, _, gap in report), report
 
 
 @pytest.mark.parametrize("d,heads,dec", [(256, 4, 1), (512, 4, 2), (512, 2, 1), (512, 8, 1),

@@ -497,11 +497,57 @@ def main():
                       out_len=pin_len.numpy(), out_off=off, beam=BEAM)
         return n_ids * 4 + (hi - lo + 1) * 8 + (hi - lo) * 8, int(b.sum()) * 4 + (hi - lo) * 4
 
+    # N > 1: the step's result is the corpus-ordered output on rank 0.  Every
+    # rank's chunk (flat ids at budget offsets + lengths, fixed-size buffers)
+    # is gathered to rank 0 (NCCL over NVLink, or gloo host tensors in a dry
+    # run) and placed at the chunk's corpus position — restore_order
+    # (batching.py:112-122) for chunk-sharded work; the native call already
+    # restored order inside each chunk.
+    gather_dev = torch.device("cpu") if backend == "gloo" else device
+    corpus_off = np.zeros(CORPUS + 1, np.int64)
+    if world > 1:
+        np.cumsum(budgets_of(lengths, 1.5, 5, cfg.max_positions), out=corpus_off[1:])
+        g_ids = torch.empty(max_out, dtype=torch.int32, device=gather_dev)
+        g_len = torch.empty(C, dtype=torch.int32, device=gather_dev)
+        if rank == 0:
+            corpus_out = torch.empty(int(corpus_off[-1]), dtype=torch.int32).pin_memory()
+            corpus_len = torch.empty(CORPUS, dtype=torch.int32).pin_memory()
+            r_ids = [torch.empty_like(g_ids) for _ in range(world)]
+            r_len = [torch.empty_like(g_len) for _ in range(world)]
+
+    def gather_step(i):
+        """Returns (h2d, d2h) bytes this rank moved for the gather."""
+        g_ids.copy_(pin_out[:max_out], non_blocking=True)
+        g_len.copy_(pin_len, non_blocking=True)
+        dist.gather(g_ids, r_ids if rank == 0 else None, dst=0)
+        dist.gather(g_len, r_len if rank == 0 else None, dst=0)
+        h = (max_out + C) * 4 if gather_dev.type == "cuda" else 0
+        if rank != 0:
+            return h, 0
+        moved = 0
+        for r in range(world):
+            cr = (r + (W + i) * world) % n_chunks
+            lo, hi, L, b, off = chunk_meta[cr]
+            nb = int(b.sum())
+            base = int(corpus_off[lo])
+            corpus_out[base:base + nb].copy_(r_ids[r][:nb], non_blocking=True)
+            corpus_len[lo:hi].copy_(r_len[r][:hi - lo], non_blocking=True)
+            moved += (nb + hi - lo) * 4
+        torch.cuda.current_stream(device).synchronize()
+        for r in range(world):
+            lo, hi = chunk_meta[(r + (W + i) * world) % n_chunks][:2]
+            gathered[0] += int(corpus_len[lo:hi].sum())
+        return h, moved if gather_dev.type == "cuda" else 0
+
     # warm the host path on every chunk the timed loop will use: the C ABI's
     # device staging buffers grow to the largest chunk here, not inside the
     # timed region (a cudaMalloc there cost up to 30% of an e2e step)
     for c in sorted({chunk_of(W + i) for i in range(K)}):
         host_step(c)
+    gathered = [0]
+    if world > 1:
+        gather_step(0)
+        gathered[0] = 0
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -514,6 +560,10 @@ def main():
         h2d += a
         d2h += bb
         e2e_words += int(pin_len[:chunk_meta[c][1] - chunk_meta[c][0]].sum())
+        if world > 1:
+            a, bb = gather_step(i)
+            h2d += a
+            d2h += bb
     e1.record()
     torch.cuda.synchronize()
     e_el = e0.elapsed_time(e1) / 1e3
@@ -522,6 +572,11 @@ def main():
            "d2h_bytes_per_step": d2h // max(K, 1),
            # same chunks through both paths: the word counts must agree exactly
            "matches_device_path": bool(e2e_words == int(words))}
+    if world > 1:
+        # rank 0 holds every rank's outputs in corpus order after each step
+        e2e["gathered_to_rank0"] = {"words": gathered[0] if rank == 0 else None,
+                                    "matches_all_ranks": bool(rank != 0 or
+                                                              gathered[0] == int(e_words_all))}
 
     peak_alloc = torch.cuda.max_memory_allocated(device)
     engine_bytes = eng.device_bytes()

@@ -165,6 +165,16 @@ int fnmt_engine_reserve(fnmt_engine* e, const fnmt_run* run);
 int64_t fnmt_budgets(const int32_t* lengths, int n, double ratio, int offset, int max_positions,
                      int32_t* budgets);
 
+/* The scheduler's batch plan, host only (no GPU needed): plan_batches
+ * (batching.py:100-109) — stable length-descending order, greedy maximal
+ * batches under count <= sbatch and count * longest <= wbatch.  Writes the
+ * sorted sentence order perm[n] (batching.py:68-70's permutation) and, per
+ * batch, sizes[] / max_len[] / oversize[] (arrays of capacity n; max_len and
+ * oversize may be NULL).  Returns the batch count (or <0).  This is the
+ * planner fnmt_engine_translate runs internally. */
+int fnmt_plan_batches(const int32_t* lengths, int n, int sbatch, int wbatch, int32_t* perm,
+                      int32_t* sizes, int32_t* max_len, uint8_t* oversize);
+
 /* Corpus-level greedy translation (greedy_translate over plan_batches,
  * batching.py:100-122 + search.py:58-86), HOST buffers:
  *   src ids for sentence i at ids[offsets[i] .. offsets[i+1]) (offsets n+1);

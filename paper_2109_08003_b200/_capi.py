@@ -72,6 +72,7 @@ _SIGNATURES = {
     "fnmt_engine_finalize": (_I, [_VP]),
     "fnmt_engine_reserve": (_I, [_VP, C.POINTER(fnmt_run)]),
     "fnmt_budgets": (_I64, [_VP, _I, C.c_double, _I, _I, _VP]),
+    "fnmt_plan_batches": (_I, [_VP, _I, _I, _I, _VP, _VP, _VP, _VP]),
     "fnmt_engine_translate": (_I, [_VP, _VP, _VP, _I, C.POINTER(fnmt_run), _VP, _VP, _VP,
                                    C.POINTER(fnmt_stats)]),
     "fnmt_engine_translate_device": (_I, [_VP, _VP, _VP, _VP, _I, C.POINTER(fnmt_run), _VP, _VP,

@@ -334,6 +334,25 @@ int64_t fnmt_budgets(const int32_t* lengths, int n, double ratio, int offset, in
   return total;
 }
 
+int fnmt_plan_batches(const int32_t* lengths, int n, int sbatch, int wbatch, int32_t* perm,
+                      int32_t* sizes, int32_t* max_len, uint8_t* oversize) {
+  if ((!lengths && n) || n < 0 || sbatch < 1 || wbatch < 1 || (n && (!perm || !sizes))) {
+    fnmt::set_error("fnmt_plan_batches: bad arguments");
+    return FNMT_E_INVALID;
+  }
+  std::vector<int32_t> L(lengths, lengths + n);
+  const auto plan = fnmt::plan_batches(L, sbatch, wbatch);
+  int k = 0, j = 0;
+  for (const auto& b : plan) {
+    for (int32_t r : b.rows) perm[j++] = r;
+    sizes[k] = (int32_t)b.rows.size();
+    if (max_len) max_len[k] = b.max_len;
+    if (oversize) oversize[k] = b.oversize ? 1 : 0;
+    ++k;
+  }
+  return k;
+}
+
 int fnmt_engine_translate_device(fnmt_engine* e, const int32_t* d_ids, const int64_t* d_offsets,
                                  const int32_t* lengths, int n, const fnmt_run* run,
                                  int32_t* d_out_ids, const int64_t* out_off,

@@ -2,13 +2,18 @@
 the corpus is sharded across ranks with no data-path collective.
 
 * ``shard_indices`` — length-sort the corpus once (the stable descending
-  order of batching.py:68-70) and deal sentences round-robin, so every rank
-  gets the same length mix (equal work per GPU, no straggler rank).
-* ``translate_distributed`` — inside an initialised ``torch.distributed``
-  group (one process per GPU, NCCL or gloo), every rank translates its shard
-  with its own engine, then the per-rank outputs are gathered with a single
-  object gather to ``dst`` and put back in corpus order (batching.py:112-122).
-  The gather is host-side result collection, not part of the hot path.
+  order of batching.py:68-70, the permutation the native planner
+  ``fnmt_plan_batches`` produces) and deal sentences round-robin, so every
+  rank gets the same length mix (equal work per GPU, no straggler rank).
+* ``gather_flat`` — result collection after the hot path: every rank holds
+  its outputs as one flat int32 id buffer plus per-sentence lengths; two
+  tensor collectives (lengths, then the id buffers padded to the largest
+  rank's total) bring them to ``dst`` and a vectorised segment permutation
+  puts them in corpus order (batching.py:112-122 ``restore_order``).  On an
+  NCCL group the buffers move as device tensors over NVLink; on gloo as host
+  tensors.  No pickling: a 1 M-sentence corpus is ~41 M int32 ids.
+* ``translate_distributed`` — the list-of-lists convenience wrapper the
+  reference's callers expect.
 """
 
 from __future__ import annotations
@@ -39,6 +44,76 @@ def restore(shards: Sequence[np.ndarray], outputs: Sequence[Sequence], n: int) -
     return res
 
 
+def restore_flat(shards: Sequence[np.ndarray], ids: Sequence[np.ndarray],
+                 lens: Sequence[np.ndarray], n: int):
+    """Flat form of :func:`restore`: rank r's sentence ``shards[r][j]`` has
+    ``lens[r][j]`` ids, stored back to back in ``ids[r]``.  Returns
+    ``(out_ids, out_off)`` in corpus order (``out_off`` has n + 1 entries)."""
+    sent = np.concatenate([np.asarray(s, np.int64) for s in shards]) if shards else \
+        np.zeros(0, np.int64)
+    ln = np.concatenate([np.asarray(x, np.int64) for x in lens]) if lens else np.zeros(0, np.int64)
+    if len(sent) != n or len(ln) != n or not np.array_equal(np.sort(sent), np.arange(n)):
+        raise ValueError("shards do not cover every sentence exactly once")
+    for s, x, L in zip(shards, ids, lens):
+        if len(s) != len(L) or int(np.sum(L)) > len(x):
+            raise ValueError("shard output count does not match its index list")
+    cat = np.concatenate([np.asarray(x[:int(np.sum(L))], np.int32) for x, L in zip(ids, lens)]) \
+        if ids else np.zeros(0, np.int32)
+    start_r = np.zeros(n, np.int64)
+    np.cumsum(ln[:-1], out=start_r[1:])            # start of each sentence in rank order
+    where = np.empty(n, np.int64)
+    where[sent] = np.arange(n)                     # corpus sentence -> rank-order slot
+    len_c = ln[where]
+    off = np.zeros(n + 1, np.int64)
+    np.cumsum(len_c, out=off[1:])
+    src = np.repeat(start_r[where] - off[:-1], len_c) + np.arange(off[-1])
+    return cat[src], off
+
+
+def gather_flat(out_ids, out_len, lengths: Sequence[int], group=None, dst: Optional[int] = 0):
+    """Collect every rank's flat outputs (``out_ids`` int32 back to back,
+    ``out_len`` int32 per sentence of this rank's shard, in shard order;
+    numpy or torch) and return ``(ids, off)`` in corpus order on ``dst``
+    (every rank if ``dst`` is None); other ranks get None."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    dev = torch.device("cuda", torch.cuda.current_device()) \
+        if dist.get_backend(group) == "nccl" else torch.device("cpu")
+    shards = [shard_indices(lengths, world, r) for r in range(world)]
+    L = torch.as_tensor(np.asarray(out_len, np.int32) if not torch.is_tensor(out_len) else out_len,
+                        dtype=torch.int32).to(dev)
+    if L.numel() != len(shards[rank]):
+        raise ValueError("out_len must hold one length per sentence of this rank's shard")
+    total = torch.tensor([int(L.sum())], dtype=torch.int64, device=dev)
+    totals = [torch.zeros_like(total) for _ in range(world)]
+    dist.all_gather(totals, total, group=group)
+    cap = max(1, max(int(t.item()) for t in totals))
+    buf = torch.zeros(cap, dtype=torch.int32, device=dev)
+    src = out_ids if torch.is_tensor(out_ids) else torch.from_numpy(np.asarray(out_ids, np.int32))
+    buf[:int(total.item())] = src[:int(total.item())].to(dev, torch.int32)
+    sizes = [len(s) for s in shards]
+    Lp = torch.zeros(max(sizes), dtype=torch.int32, device=dev)
+    Lp[:L.numel()] = L
+    if dst is None:
+        ids_all = [torch.empty_like(buf) for _ in range(world)]
+        len_all = [torch.empty_like(Lp) for _ in range(world)]
+        dist.all_gather(ids_all, buf, group=group)
+        dist.all_gather(len_all, Lp, group=group)
+    else:
+        me = rank == dst
+        ids_all = [torch.empty_like(buf) for _ in range(world)] if me else None
+        len_all = [torch.empty_like(Lp) for _ in range(world)] if me else None
+        dist.gather(buf, ids_all, dst=dst, group=group)
+        dist.gather(Lp, len_all, dst=dst, group=group)
+        if not me:
+            return None
+    ids_np = [t.cpu().numpy() for t in ids_all]
+    len_np = [t.cpu().numpy()[:sizes[r]] for r, t in enumerate(len_all)]
+    return restore_flat(shards, ids_np, len_np, len(lengths))
+
+
 def translate_distributed(translate_fn: Callable[[list], list], rows: Sequence, group=None,
                           dst: Optional[int] = 0) -> Optional[list]:
     """Translate ``rows`` (list of id sequences, identical on every rank)
@@ -51,12 +126,13 @@ def translate_distributed(translate_fn: Callable[[list], list], rows: Sequence, 
     lengths = [len(r) for r in rows]
     mine = shard_indices(lengths, world, rank)
     outs = translate_fn([rows[int(i)] for i in mine])
-    gathered = [None] * world
-    if dst is None:
-        dist.all_gather_object(gathered, outs, group=group)
-    else:
-        dist.gather_object(outs, gathered if rank == dst else None, dst=dst, group=group)
-        if rank != dst:
-            return None
-    shards = [shard_indices(lengths, world, r) for r in range(world)]
-    return restore(shards, gathered, len(rows))
+    if len(outs) != len(mine):
+        raise ValueError("translate_fn returned a different number of outputs")
+    ln = np.array([len(o) for o in outs], np.int32)
+    flat = np.concatenate([np.asarray(o, np.int32) for o in outs]) if len(outs) else \
+        np.zeros(0, np.int32)
+    got = gather_flat(flat, ln, lengths, group=group, dst=dst)
+    if got is None:
+        return None
+    ids, off = got
+    return [ids[off[i]:off[i + 1]].tolist() for i in range(len(rows))]

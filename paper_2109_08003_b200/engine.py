@@ -42,6 +42,28 @@ def budgets_of(lengths: np.ndarray, ratio: float, offset: int, max_positions: in
     return out
 
 
+def native_plan(lengths, sbatch: int, wbatch: int):
+    """The native scheduler's batch plan (``fnmt_plan_batches``, host only):
+    returns ``(permutation, batches)`` with ``batches`` a list of
+    ``(indices, max_len, oversize)`` — the shape of ``batching.plan_batches``
+    (batching.py:100-109), so the planner ``fnmt_engine_translate`` runs can be
+    checked against the reference's fixtures without a GPU."""
+    lengths = np.ascontiguousarray(lengths, dtype=np.int32)
+    n = len(lengths)
+    perm = np.empty(max(n, 1), np.int32)
+    sizes = np.empty(max(n, 1), np.int32)
+    mlen = np.empty(max(n, 1), np.int32)
+    over = np.empty(max(n, 1), np.uint8)
+    k = check(lib.fnmt_plan_batches(lengths.ctypes.data, n, int(sbatch), int(wbatch),
+                                    perm.ctypes.data, sizes.ctypes.data, mlen.ctypes.data,
+                                    over.ctypes.data), "plan_batches")
+    batches, j = [], 0
+    for b in range(k):
+        batches.append((perm[j:j + sizes[b]].tolist(), int(mlen[b]), bool(over[b])))
+        j += int(sizes[b])
+    return perm[:n].tolist(), batches
+
+
 def stats_dict(st: _capi.fnmt_stats) -> dict:
     return {name: getattr(st, name) for name, _ in st._fields_}
 

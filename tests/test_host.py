@@ -126,6 +126,46 @@ def test_batching_fuzz_against_oracle(seed):
     assert B.estimate_peak_memory(plan, cfg, 40) == O.peak_bytes(batches, O.arch_of(cfg), 40)
 
 
+def test_native_planner_matches_reference_golden(golden):
+    """The planner the product runs (engine.cu plan_batches via the C ABI)
+    against the reference's recorded plans (batching.py:100-109)."""
+    from paper_2109_08003_b200.engine import native_plan
+    g = golden("batching")
+    for i in range(6):
+        lengths = [int(x) for x in g[f"c{i}_lengths"]]
+        sb, wb = (int(x) for x in g[f"c{i}_caps"])
+        perm, batches = native_plan(lengths, sb, wb)
+        assert perm == [int(x) for x in g[f"c{i}_perm"]]
+        assert [len(b[0]) for b in batches] == [int(x) for x in g[f"c{i}_sizes"]]
+        assert [b[1] for b in batches] == [int(x) for x in g[f"c{i}_maxlen"]]
+        assert [b[2] for b in batches] == [bool(x) for x in g[f"c{i}_oversize"]]
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_native_planner_fuzz_against_oracle(seed):
+    from paper_2109_08003_b200.engine import native_plan
+    rng = np.random.default_rng(100 + seed)
+    lengths = [int(x) for x in rng.integers(1, 300, size=int(rng.integers(0, 200)))]
+    sb, wb = int(rng.integers(1, 40)), int(rng.integers(8, 2000))
+    perm, batches = native_plan(lengths, sb, wb)
+    want, wperm = O.plan(lengths, sb, wb)
+    assert perm == wperm
+    assert batches == [(list(b[0]), b[1], b[2]) for b in want]
+
+
+def test_native_planner_corpus_scale():
+    """At the bench's caps over a 65 536-sentence newstest-shaped chunk the
+    native plan equals the Python restatement batch for batch."""
+    from paper_2109_08003_b200.engine import native_plan
+    from paper_2109_08003_b200.synthetic import newstest_lengths
+    lengths = newstest_lengths(65536)
+    perm, batches = native_plan(lengths, 3072, 64000)
+    plan = B.plan_batches([int(x) for x in lengths], B.DecodeLimits(sbatch=3072, wbatch=64000))
+    assert perm == list(plan.permutation)
+    assert [(b[0], b[1], b[2]) for b in batches] == \
+        [(list(b.indices), b.max_len, b.oversize) for b in plan.batches]
+
+
 def test_restore_order_integrity():
     plan = B.plan_batches([4, 4], B.DecodeLimits())
     with pytest.raises(B.IntegrityError):

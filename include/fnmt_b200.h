@@ -235,6 +235,13 @@ int fnmt_engine_profile(fnmt_engine* e, int enable);
 int fnmt_engine_profile_read(fnmt_engine* e, double* ms, int64_t* launches, double* flops,
                              double* bytes);
 
+/* Every launch of the profiled runs in launch order: kernel class, event
+ * time (ms) and the algorithmic FLOPs / bytes counted for it.
+ * Writes min(cap, count) entries (any pointer may be NULL) and returns the
+ * count; lets a per-launch ncu DRAM-bytes list be matched launch by launch. */
+int64_t fnmt_engine_profile_log(fnmt_engine* e, int32_t* cls, float* ms, double* flops,
+                                double* bytes, int64_t cap);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

@@ -85,6 +85,7 @@ _SIGNATURES = {
     "fnmt_engine_set_lanes": (_I, [_VP, _I]),
     "fnmt_engine_stream": (_VP, [_VP]),
     "fnmt_engine_profile": (_I, [_VP, _I]),
+    "fnmt_engine_profile_log": (_I64, [_VP, _VP, _VP, _VP, _VP, _I64]),
     "fnmt_engine_profile_read": (_I, [_VP, _VP, _VP, _VP, _VP]),
 }
 

@@ -476,6 +476,20 @@ int fnmt_engine_profile_read(fnmt_engine* e, double* ms, int64_t* launches, doub
   return FNMT_OK;
 }
 
+int64_t fnmt_engine_profile_log(fnmt_engine* e, int32_t* cls, float* ms, double* flops,
+                                double* bytes, int64_t cap) {
+  if (!e || cap < 0) return fail(FNMT_E_INVALID, "profile_log: bad arguments");
+  const auto& log = e->eng->prof_log;
+  const int64_t n = std::min<int64_t>(cap, (int64_t)log.size());
+  for (int64_t i = 0; i < n; ++i) {
+    if (cls) cls[i] = log[i].cls;
+    if (ms) ms[i] = log[i].ms;
+    if (flops) flops[i] = log[i].flops;
+    if (bytes) bytes[i] = log[i].bytes;
+  }
+  return (int64_t)log.size();
+}
+
 int64_t fnmt_engine_device_bytes(const fnmt_engine* e) {
   return e ? e->eng->total_device_bytes() : 0;
 }

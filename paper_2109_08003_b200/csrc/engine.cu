@@ -208,6 +208,7 @@ void Engine::set_profiling(bool on) {
   profiling = on;
   prof_used = 0;
   prof_recs.clear();
+  prof_log.clear();
   for (int i = 0; i < FNMT_K_COUNT; ++i) {
     prof_ms[i] = prof_flops[i] = prof_bytes[i] = 0.0;
     prof_n[i] = 0;
@@ -243,6 +244,7 @@ void Engine::prof_collect() {
     prof_n[r.cls] += 1;
     prof_flops[r.cls] += r.flops;
     prof_bytes[r.cls] += r.bytes;
+    prof_log.push_back(ProfLog{r.cls, ms, r.flops, r.bytes});
   }
   prof_recs.clear();
   prof_used = 0;

@@ -214,6 +214,14 @@ class Engine {
   int64_t prof_n[FNMT_K_COUNT] = {};
   double prof_flops[FNMT_K_COUNT] = {};
   double prof_bytes[FNMT_K_COUNT] = {};
+  // every profiled launch in launch order (class, event ms, algorithmic counts):
+  // matched launch by launch against an ncu DRAM-bytes list of the same run
+  struct ProfLog {
+    int cls;
+    float ms;
+    double flops, bytes;
+  };
+  std::vector<ProfLog> prof_log;
 
  private:
   int prof_begin(cudaStream_t s);

@@ -151,6 +151,18 @@ class Engine:
                 for i, name in enumerate(_capi.KERNEL_CLASSES)}
 
 
+    def profile_log(self) -> dict:
+        """Per-launch log of the profiled runs (launch order): numpy arrays
+        ``cls`` (index into KERNEL_CLASSES), ``ms``, ``flops``, ``bytes``."""
+        n = check(lib.fnmt_engine_profile_log(self.handle.h, None, None, None, None, 0),
+                  "profile_log")
+        out = {"cls": np.empty(n, np.int32), "ms": np.empty(n, np.float32),
+               "flops": np.empty(n, np.float64), "bytes": np.empty(n, np.float64)}
+        check(lib.fnmt_engine_profile_log(self.handle.h, out["cls"].ctypes.data,
+                                          out["ms"].ctypes.data, out["flops"].ctypes.data,
+                                          out["bytes"].ctypes.data, n), "profile_log")
+        return out
+
 def translate_ids(handle, rows, search=None, sbatch=3072, wbatch=64000) -> list[list[int]]:
     """Translate a list of id sequences through the native corpus path (greedy,
     or batched beam when search.beam_size > 1)."""

@@ -826,6 +826,7 @@ void Engine::run_step(const StepView& v, cudaStream_t s) {
   ++launches;
   for (int l = 0; l < arch.n_dec_layers; ++l) {
     const DecL& L = dec[l];
+    bool layer_fused = false;
     if (fused_self && v.ws_caches && !v.anc) {
       // folded self attention: this step's [K~ | V~ | c] row straight into cache
       // slot t; the query is the layer input itself and the attention writes the
@@ -853,6 +854,45 @@ void Engine::run_step(const StepView& v, cudaStream_t s) {
       CK(launch_gemm(g, s));
       prof_end(s, ev, gemm_cls, 2.0 * Rl * fl * d, Rl * d * es + (double)fl * d * es + Rl * fl * es);
       ++launches;
+      if (fused_cross && dec_layer_fused_ok(dt, d, arch.n_heads_dec)) {
+        // one kernel: self attention, + residual, norm1, cross attention, + residual, norm2
+        DecLayerArgs f{};
+        f.q = ws.dxa;
+        f.ldq = d;
+        f.x32 = ws.dx32;
+        f.xa = ws.dxa;
+        f.kself = v.kc[l];
+        f.ld_self = fl;
+        f.cap = v.cap;
+        f.t_ptr = v.t_ptr;
+        f.kcross = v.ckv[l];
+        f.ld_cross = ckv_ld;
+        f.k_start = v.k_start;
+        f.k_len = v.k_len;
+        f.k_pad = v.k_pad;
+        f.rows_per_seq = v.rows_per_seq;
+        f.voff = d;
+        f.kc_off = 2 * d;
+        f.bo_self = L.so.b;
+        f.g1 = L.n1.g;
+        f.b1 = L.n1.b;
+        f.bo_cross = L.co.b;
+        f.g2 = L.n2.g;
+        f.b2 = L.n2.b;
+        f.l1 = arch.norm_l1;
+        f.dtype = dt;
+        f.d = d;
+        f.rows = R;
+        f.row_done = v.row_done;
+        const int ev2 = prof_begin(s);
+        CK(launch_dec_layer_fused(f, s));
+        // SURVEY §8(d) attention bytes (self t+1 keys + cross S keys, 2 d each,
+        // live rows) plus the row's residual in / out and query reads
+        prof_end(s, ev2, FNMT_K_ATTN_DEC, 0.0,
+                 (Rl * (v.host_t + 1) + Sl) * 2 * d * es + Rl * d * (8.0 + 2 * es));
+        ++launches;
+        layer_fused = true;
+      } else {
       DecAttnArgs a{};
       a.q = ws.dxa;
       a.ldq = d;
@@ -880,6 +920,7 @@ void Engine::run_step(const StepView& v, cudaStream_t s) {
       }
       ++launches;
       norm(ws.dx32, ws.dy32, L.n1, ws.dx32, ws.dxa, R, s);
+      }
     } else {
     {
       // q -> ws.dq, this step's k / v straight into the self cache slot t (fused append)
@@ -943,6 +984,7 @@ void Engine::run_step(const StepView& v, cudaStream_t s) {
     ++launches;
     gemm_norm(ws.datt, tc ? &ws.tm_datt : nullptr, d, L.so, R, ws.dx32, ws.dxa, ws.dy32, L.n1, s);
     }
+    if (!layer_fused) {
     // folded cross attention (workspace caches only): q is the norm1 output itself,
     // the attention writes the o-projection output (fp32, + bias) straight into dy32
     const bool folded = fused_cross && v.ws_caches;
@@ -981,6 +1023,7 @@ void Engine::run_step(const StepView& v, cudaStream_t s) {
       norm(ws.dx32, ws.dy32, L.n2, ws.dx32, ws.dxa, R, s);
     else
       gemm_norm(ws.datt, tc ? &ws.tm_datt : nullptr, d, L.co, R, ws.dx32, ws.dxa, ws.dy32, L.n2, s);
+    }
     if (L.ffn) {
       gemm(ws.dxa, tc ? &ws.tm_dxa : nullptr, d, L.f1, R, ws.dh, arch.ffn_dim_dec, dt, 1, s);
       gemm_norm(ws.dh, tc ? &ws.tm_dh : nullptr, arch.ffn_dim_dec, L.f2, R, ws.dx32, ws.dxa, ws.dy32,

@@ -206,6 +206,26 @@ struct DecAttnArgs {
 };
 cudaError_t launch_attention_decode(const DecAttnArgs& a, cudaStream_t s);
 
+// Fused decoder attention block, single-head folded decoders (dec_layer.cu):
+// self attention over the folded self cache -> + residual -> norm1 -> cross
+// attention over the folded cross cache -> + residual -> norm2, one CTA per row.
+struct DecLayerArgs {
+  const void* q; int ldq;               // layer input (activation copy of x32)
+  float* x32;                           // [rows, d] residual stream, updated in place
+  void* xa;                             // [rows, d] activation copy of the output
+  const void* kself; int ld_self;       // folded self cache rows r*cap + j
+  int cap; const int32_t* t_ptr;
+  const void* kcross; int ld_cross;     // folded cross cache rows k_start[seq] + j
+  const int32_t* k_start; const int32_t* k_len; int k_pad; int rows_per_seq;
+  int voff, kc_off;                     // V~ and c columns inside a cached row
+  const float* bo_self; const float* g1; const float* b1;
+  const float* bo_cross; const float* g2; const float* b2;
+  int l1, dtype, d, rows;
+  const uint8_t* row_done;
+};
+bool dec_layer_fused_ok(int dtype, int d, int heads);
+cudaError_t launch_dec_layer_fused(const DecLayerArgs& a, cudaStream_t s);
+
 // ---------------------------------------------------------------------------
 // search bookkeeping (search.py:58-86)
 

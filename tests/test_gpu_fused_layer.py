@@ -1,0 +1,62 @@
+"""The fused decoder attention block (dec_layer.cu: self attention + norm1 +
+cross attention + norm2 in one kernel, single-head folded decoders) against
+the unfused launch sequence (bulk decode attention + add_norm kernels,
+FNMT_FUSED_LAYER=0 in a subprocess) on the benchmarked workload: corpus
+chunk 0 of the newstest-shaped corpus, Student-6-1-1, caps 3072/64000.  Same
+chunking of the online softmax and the same norm arithmetic, so the token
+ids are expected to be identical; the oracle-level bar is covered by
+test_gpu_corpus_parity.py, which runs this kernel by default."""
+
+import json
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+ROOT = Path(__file__).resolve().parent.parent
+N = 8192
+SCRIPT = r"""
+import sys, json, numpy as np
+sys.path.insert(0, sys.argv[1])
+from paper_2109_08003_b200 import store as S
+from paper_2109_08003_b200.engine import Engine
+from paper_2109_08003_b200.synthetic import newstest_corpus
+cfg = S.ModelConfig(6, 1, 512, 1, 1, 2048, 2048, 32772, 1024)
+ids, off, _ = newstest_corpus(1 << 20, 32772)
+n = int(sys.argv[2])
+eng = Engine(cfg, S.random_model(cfg, 0), dtype=sys.argv[3])
+out, olen, oof, st = eng.translate(ids, off[:n + 1], sbatch=3072, wbatch=64000)
+np.savez(sys.argv[4], out=out, olen=olen, oof=oof)
+print(json.dumps({"launches": int(st.gpu_launches)}))
+"""
+
+
+def run(tmp_path, dtype, fused):
+    env = dict(os.environ, FNMT_FUSED_LAYER="1" if fused else "0")
+    f = tmp_path / f"{dtype}_{int(fused)}.npz"
+    r = subprocess.run([sys.executable, "-c", SCRIPT, str(ROOT), str(N), dtype, str(f)], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    st = json.loads(r.stdout.strip().splitlines()[-1])
+    d = np.load(f)
+    rows = [d["out"][d["oof"][i]:d["oof"][i] + d["olen"][i]].tolist() for i in range(N)]
+    return rows, st["launches"]
+
+
+@pytest.mark.parametrize("dtype", ["f16", "bf16"])
+def test_fused_layer_matches_unfused_sequence(tmp_path, dtype):
+    a, la = run(tmp_path, dtype, True)
+    b, lb = run(tmp_path, dtype, False)
+    same = sum(x == y for x, y in zip(a, b))
+    print(dtype, "fused vs unfused identical:", same, "/", N, "launches", la, "vs", lb)
+    assert same >= N - 2        # same arithmetic: identical up to a stray f64-sum ulp
+    assert la < lb              # three launches per decode step fewer

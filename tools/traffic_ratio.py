@@ -39,7 +39,7 @@ def read_ncu(path):
 
 def group_of_name(name):
     n = name.split("(")[0].split("<")[0].split("::")[-1].strip()
-    for pre, g in (("attn_dec", "attn_dec"), ("attn_varlen", "attn_enc"), ("add_norm", "norm"),
+    for pre, g in (("attn_dec", "attn_dec"), ("dec_layer", "attn_dec"), ("attn_varlen", "attn_enc"), ("add_norm", "norm"),
                    ("embed", "embed"), ("greedy_update", "search"), ("beam_row_reduce", "search"),
                    ("beam_select", "search"), ("gemm_", "gemm")):
         if n.startswith(pre):

@@ -243,6 +243,223 @@ __global__ void __launch_bounds__(kMThreads)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Pipelined variant for short sequences (<= 64 keys: the newstest batches).
+// Same arithmetic as attn_varlen_mma_kernel (fragment order, fp32 scores,
+// softmax, P rounded to T, identical outputs), but the operands stream
+// through a 3-stage cp.async ring of head-dim chunks instead of synchronous
+// loads: chunks 0..nd-1 carry the (Q, K) columns [64c, 64c+64) of the
+// sequence, chunks nd..2nd-1 the V columns; while chunk c is in the tensor
+// cores chunks c+1 and c+2 are in flight (the V chunks already load during
+// the softmax).  Stages hold only the sequence's rows (RQ queries, RK keys,
+// rounded to 16), so several CTAs share an SM.
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// rows [0, n) of the 64-column chunk c0 of a row-major matrix into a stage
+// region (row stride kLds); columns past dk are zero-filled (plain stores)
+template <typename T>
+__device__ __forceinline__ void stage_async(T* dst, const T* src, int64_t row0, int ld, int n,
+                                            int c0, int dk) {
+  for (int i = threadIdx.x; i < n * (kMD / 8); i += kMThreads) {
+    const int r = i >> 3, c8 = (i & 7) * 8;
+    if (c0 + c8 < dk)
+      cp_async16(dst + r * kLds + c8, src + (row0 + r) * ld + c0 + c8);
+    else
+      *reinterpret_cast<uint4*>(dst + r * kLds + c8) = make_uint4(0u, 0u, 0u, 0u);
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kMThreads)
+    attn_enc_pipe_kernel(AttnArgs a, float qscale, int RQ, int RK) {
+  extern __shared__ __align__(16) uint8_t smraw[];
+  const int scap = RK + 4;                              // fp32 score row stride
+  float* S = reinterpret_cast<float*>(smraw);           // [RQ][scap]
+  T* ring = reinterpret_cast<T*>(S + RQ * scap);        // 3 x [(RQ + RK) x kLds]
+  const int stage_elems = (RQ + RK) * kLds;
+  const int b = blockIdx.y, h = blockIdx.z;
+  const int q0 = blockIdx.x * kMQ;
+  const int nq = a.q_len[b];
+  if (q0 >= nq) return;
+  const int kl = a.k_len[b];
+  const bool all_masked = kl == 0;
+  const int nk = all_masked ? a.k_pad : kl;
+  const int nk16 = (nk + 15) & ~15;
+  const int qn = min(kMQ, nq - q0);
+  const int64_t qrow0 = a.q_start[b] + q0;
+  const int64_t krow0 = a.k_start[b];
+  const int dk = a.dk;
+  const int nd = (dk + kMD - 1) / kMD;
+  const T* q = reinterpret_cast<const T*>(a.q) + h * dk;
+  const T* k = reinterpret_cast<const T*>(a.k) + h * dk;
+  const T* v = reinterpret_cast<const T*>(a.v) + h * dk;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, tig = lane & 3;
+  const int wr = warp * 16;
+  const bool live = wr < qn;
+  const int ntk = nk16 >> 3;                            // 8-key score tiles in use
+
+  auto load = [&](int c) {
+    if (c < 2 * nd) {
+      T* st = ring + (c % 3) * stage_elems;
+      if (c < nd) {
+        stage_async(st, q, qrow0, a.ldq, qn, c * kMD, dk);
+        stage_async(st + RQ * kLds, k, krow0, a.ldkv, nk, c * kMD, dk);
+      } else {
+        stage_async(st, v, krow0, a.ldkv, nk, (c - nd) * kMD, dk);
+        // value rows [nk, nk16) meet zero probabilities: make them finite
+        for (int i = threadIdx.x; i < (nk16 - nk) * (kMD / 8); i += kMThreads)
+          *reinterpret_cast<uint4*>(st + (nk + (i >> 3)) * kLds + (i & 7) * 8) =
+              make_uint4(0u, 0u, 0u, 0u);
+      }
+    }
+    cp_async_commit();
+  };
+  load(0);
+  load(1);
+
+  float acc[8][4];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
+  T* out = reinterpret_cast<T*>(a.out) + h * dk;
+  for (int c = 0; c < 2 * nd; ++c) {
+    cp_async_wait<1>();
+    __syncthreads();
+    load(c + 2);
+    const T* st = ring + (c % 3) * stage_elems;
+    if (c < nd) {
+      // ---- scores over head-dim chunk c ----
+      if (live) {
+        const T* Qs = st;
+        const T* Ks = st + RQ * kLds;
+#pragma unroll
+        for (int kk = 0; kk < kMD; kk += 16) {
+          uint32_t af[4];
+          const T* qa = Qs + (wr + g) * kLds + kk + 2 * tig;
+          af[0] = lds32(qa);
+          af[1] = lds32(qa + 8 * kLds);
+          af[2] = lds32(qa + 8);
+          af[3] = lds32(qa + 8 * kLds + 8);
+#pragma unroll
+          for (int nt = 0; nt < 8; ++nt) {
+            if (nt < ntk) {
+              const T* kb = Ks + (nt * 8 + g) * kLds + kk + 2 * tig;
+              mma16816<T>(acc[nt], af, lds32(kb), lds32(kb + 8));
+            }
+          }
+        }
+      }
+      if (c == nd - 1) {
+        if (live) {
+#pragma unroll
+          for (int nt = 0; nt < 8; ++nt)
+            if (nt < ntk)
+#pragma unroll
+              for (int hh = 0; hh < 2; ++hh) {
+                const int qi = wr + g + 8 * hh;
+                const int kj = nt * 8 + 2 * tig;
+                float s0 = acc[nt][2 * hh] * qscale, s1 = acc[nt][2 * hh + 1] * qscale;
+                if (all_masked) {
+                  s0 += kMaskValue;
+                  s1 += kMaskValue;
+                }
+                *reinterpret_cast<float2*>(S + qi * scap + kj) = make_float2(s0, s1);
+              }
+        }
+        __syncthreads();
+        // softmax (tensor.py:70-81); probabilities of keys [nk, nk16) are zero
+        for (int qi = warp; qi < RQ; qi += kMThreads / 32) {
+          float* pr = S + qi * scap;
+          if (qi >= qn) {
+            for (int j = lane; j < nk16; j += 32) pr[j] = 0.f;
+            continue;
+          }
+          float mx = -INFINITY;
+          for (int j = lane; j < nk; j += 32) mx = fmaxf(mx, pr[j]);
+          mx = warp_max(mx);
+          float sum = 0.f;
+          for (int j = lane; j < nk; j += 32) {
+            const float e = expf(pr[j] - mx);
+            pr[j] = e;
+            sum += e;
+          }
+          sum = warp_sum(sum);
+          for (int j = lane; j < nk; j += 32) pr[j] = pr[j] / sum;
+          for (int j = nk + lane; j < nk16; j += 32) pr[j] = 0.f;
+        }
+        __syncthreads();
+      }
+    } else if (live) {
+      // ---- O[:, chunk] = P V[:, chunk] (all keys are in this stage) ----
+      const int dc = (c - nd) * kMD;
+      float o[8][4];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+      for (int kk = 0; kk < nk16; kk += 16) {
+        const float* p0 = S + (wr + g) * scap + kk + 2 * tig;
+        const float* p1 = p0 + 8 * scap;
+        uint32_t af[4];
+        af[0] = pack2<T>(p0[0], p0[1]);
+        af[1] = pack2<T>(p1[0], p1[1]);
+        af[2] = pack2<T>(p0[8], p0[9]);
+        af[3] = pack2<T>(p1[8], p1[9]);
+        const int mi = lane >> 3;
+        const int key = kk + (lane & 7) + ((mi & 1) ? 8 : 0);
+#pragma unroll
+        for (int nt = 0; nt < 8; nt += 2) {
+          uint32_t bf[4];
+          ldmatrix_x4_trans(bf, st + key * kLds + nt * 8 + ((mi & 2) ? 8 : 0));
+          mma16816<T>(o[nt], af, bf[0], bf[1]);
+          mma16816<T>(o[nt + 1], af, bf[2], bf[3]);
+        }
+      }
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const int qi = wr + g + 8 * hh;
+          const int dd = dc + nt * 8 + 2 * tig;
+          if (qi < qn && dd < dk)
+            *reinterpret_cast<uint32_t*>(out + (qrow0 + qi) * a.ldo + dd) =
+                pack2<T>(o[nt][2 * hh], o[nt][2 * hh + 1]);
+        }
+    }
+  }
+  cp_async_wait<0>();
+}
+
+bool enc_pipe_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("FNMT_ATTN_PIPE");
+    on = !(e && e[0] == '0');
+  }
+  return on != 0;
+}
+
+template <typename T>
+cudaError_t pipe_dispatch(const AttnArgs& a, cudaStream_t s) {
+  const int RQ = std::min(kMQ, (a.max_q + 15) & ~15);
+  const int RK = (a.max_k + 15) & ~15;
+  const size_t smem = sizeof(float) * (size_t)RQ * (RK + 4) +
+                      sizeof(T) * 3 * (size_t)(RQ + RK) * kLds;
+  cudaError_t e = set_max_smem((const void*)attn_enc_pipe_kernel<T>);
+  if (e != cudaSuccess) return e;
+  dim3 grid((a.max_q + kMQ - 1) / kMQ, a.n_seq, a.heads);
+  const float qscale = (float)(1.0 / sqrt((double)a.dk));
+  attn_enc_pipe_kernel<T><<<grid, kMThreads, smem, s>>>(a, qscale, RQ, RK);
+  return cudaGetLastError();
+}
+
 template <typename T>
 cudaError_t mma_dispatch(const AttnArgs& a, cudaStream_t s) {
   const int scap = ((a.max_k + kMK - 1) / kMK) * kMK;
@@ -269,6 +486,8 @@ bool attention_mma_ok(const AttnArgs& a) {
 
 cudaError_t launch_attention_varlen_mma(const AttnArgs& a, cudaStream_t s) {
   if (a.n_seq <= 0 || a.max_q <= 0) return cudaSuccess;
+  if (enc_pipe_enabled() && std::max(a.max_k, a.k_pad) <= kMK)
+    return a.dtype == kF16 ? pipe_dispatch<__half>(a, s) : pipe_dispatch<__nv_bfloat16>(a, s);
   return a.dtype == kF16 ? mma_dispatch<__half>(a, s) : mma_dispatch<__nv_bfloat16>(a, s);
 }
 

@@ -30,7 +30,7 @@ def read_ncu(path):
             order.append(key)
         v = float(r["Metric Value"].replace(",", "")) if r["Metric Value"] else 0.0
         unit = r.get("Metric Unit", "")
-        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9,
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "ns": 1e-9, "us": 1e-6, "ms": 1e-3,
                  "usecond": 1e-6, "msecond": 1e-3, "second": 1.0}.get(unit, 1.0)
         rows[key]["name"] = r["Kernel Name"]
         rows[key][r["Metric Name"]] = v * scale

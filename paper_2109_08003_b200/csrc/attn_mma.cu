@@ -279,7 +279,7 @@ __device__ __forceinline__ void stage_async(T* dst, const T* src, int64_t row0, 
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kMThreads)
+__global__ void __launch_bounds__(kMThreads, 5)
     attn_enc_pipe_kernel(AttnArgs a, float qscale, int RQ, int RK) {
   extern __shared__ __align__(16) uint8_t smraw[];
   const int scap = RK + 4;                              // fp32 score row stride

@@ -240,7 +240,15 @@ __global__ void __launch_bounds__(NT) dec_layer_fused_kernel(DecLayerArgs a, flo
       const float pj = expf(S[j] - m_new);
       l_run += pj;
       const T* vr = vrow0 + (size_t)j * ld;
-      if constexpr (CPT == 4) {
+      if constexpr (CPT == 2) {
+        float2 v0;
+        if constexpr (std::is_same<T, __half>::value)
+          v0 = __half22float2(*reinterpret_cast<const __half2*>(vr));
+        else
+          v0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(vr));
+        acc[0] = fmaf(pj, v0.x, acc[0]);
+        acc[1] = fmaf(pj, v0.y, acc[1]);
+      } else if constexpr (CPT == 4) {
         const uint2 u = *reinterpret_cast<const uint2*>(vr);
         float2 v0, v1;
         if constexpr (std::is_same<T, __half>::value) {
@@ -329,6 +337,14 @@ cudaError_t launch_dec_layer_fused(const DecLayerArgs& a, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     return launch_k(kern, dim3(a.rows), dim3(nt), smem, s, a, qscale, ch_s, ch_c, buf);
   };
+  static int nt = -1;
+  if (nt < 0) {
+    const char* e = getenv("FNMT_LAYER_NT");   // 128 (4 columns / thread) or 256 (2)
+    nt = e ? atoi(e) : 128;
+  }
+  if (a.d == 512 && nt == 256)
+    return a.dtype == kF16 ? go(dec_layer_fused_kernel<__half, 256, 2>, 256)
+                           : go(dec_layer_fused_kernel<__nv_bfloat16, 256, 2>, 256);
   if (a.dtype == kF16) {
     if (a.d == 512) return go(dec_layer_fused_kernel<__half, 128, 4>, 128);
     if (a.d == 256) return go(dec_layer_fused_kernel<__half, 64, 4>, 64);

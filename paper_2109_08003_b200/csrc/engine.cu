@@ -81,6 +81,8 @@ __global__ void init_decode_kernel(int32_t* prev, uint8_t* finished, int32_t* ou
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     *t = 0;
     *alive = rows;
+    t[2] = 0;   // greedy_embed_kernel: CTA-completion counter
+    t[3] = 0;   // and alive accumulator
   }
 }
 
@@ -483,6 +485,15 @@ Lin Engine::make_folded(const std::string& p, const std::string& blk) {
   return L;
 }
 
+bool greedy_embed_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("FNMT_GREEDY_EMBED");
+    on = !(e && e[0] == '0');
+  }
+  return on != 0;
+}
+
 bool fused_self_enabled() {
   static int on = -1;
   if (on < 0) {
@@ -817,13 +828,13 @@ void Engine::run_step(const StepView& v, cudaStream_t s) {
   const double Rl = (profiling && v.prof_live) ? (double)(*v.prof_live)[v.host_t] : (double)R;
   const double Sl = (profiling && v.prof_src) ? (*v.prof_src)[v.host_t] : (double)R * v.max_k;
   prof_m = profiling ? Rl : -1.0;
-  {
+  if (!v.embed_done) {
     const int ev = prof_begin(s);
     CK(launch_embed(v.prev, nullptr, v.t_ptr, tgt_emb32, pos32, emb_scale(), ws.dx32,
                     tc ? ws.dxa : nullptr, dt, R, d, s));
     prof_end(s, ev, FNMT_K_EMBED, 0.0, Rl * d * (8.0 + dtype_size(dt)));
+    ++launches;
   }
-  ++launches;
   for (int l = 0; l < arch.n_dec_layers; ++l) {
     const DecL& L = dec[l];
     bool layer_fused = false;
@@ -1405,12 +1416,41 @@ int Engine::decode_greedy(int R, int cap, int max_len, const fnmt_run& run,
   gs.out_cap = cap;
   gs.eos = run.eos_id;
   gs.pad = run.pad_id;
+  // greedy update fused with the next step's embedding (the step graph then
+  // starts at the first decoder GEMM); the first input is embedded here
+  const bool fuse_embed = greedy_embed_enabled();
+  GreedyEmbed ge{};
+  if (fuse_embed) {
+    ge.table = tgt_emb32;
+    ge.pos = pos32;
+    ge.scale = emb_scale();
+    ge.x32 = ws.dx32;
+    ge.xa = dt == kF32 ? nullptr : ws.dxa;
+    ge.act_dtype = dt;
+    ge.d = arch.d_model;
+    ge.n_pos = arch.max_positions;
+    ge.done = ws.t + 2;
+    ge.alive_acc = ws.t + 3;
+    const int ev = prof_begin(stream);
+    CK(launch_embed(ws.prev, nullptr, ws.t, tgt_emb32, pos32, emb_scale(), ws.dx32,
+                    dt == kF32 ? nullptr : ws.dxa, dt, R, arch.d_model, stream));
+    prof_end(stream, ev, FNMT_K_EMBED, 0.0, (double)R * arch.d_model * (8.0 + dtype_size(dt)));
+    ++launches;
+    v.embed_done = true;
+  }
   auto body = [&](int t) {
     v.host_t = t;
     run_step(v, stream);
     const int ev = prof_begin(stream);
-    CK(launch_greedy_update(gs, stream));
-    prof_end(stream, ev, FNMT_K_SEARCH, 0.0, (profiling ? (double)live[t] : (double)R) * 24);
+    const double rl = profiling ? (double)live[t] : (double)R;
+    if (fuse_embed) {
+      CK(launch_greedy_embed(gs, ge, stream));
+      prof_end(stream, ev, FNMT_K_SEARCH, 0.0,
+               rl * 24 + rl * arch.d_model * (8.0 + dtype_size(dt)));
+    } else {
+      CK(launch_greedy_update(gs, stream));
+      prof_end(stream, ev, FNMT_K_SEARCH, 0.0, rl * 24);
+    }
     ++launches;
   };
   const int64_t nodes = profiling ? 0 : capture_step([&] { body(0); });

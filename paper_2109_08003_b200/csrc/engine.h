@@ -110,6 +110,8 @@ struct StepView {
   unsigned long long* keys = nullptr;  // argmax output (greedy)
   float* logits = nullptr;             // or full logits (protocol path / fp32 beam)
   const TopKPartials* topk = nullptr;  // beam: per-tile top-K partials
+  bool embed_done = false;             // the decoder input was written by the previous
+                                       // step's greedy update (greedy_embed_kernel)
 };
 
 // Host + device metadata of one translate call, shared by all lanes.

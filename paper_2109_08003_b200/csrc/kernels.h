@@ -241,6 +241,18 @@ struct GreedyState {
   int rows, out_cap, eos, pad;
 };
 cudaError_t launch_greedy_update(const GreedyState& g, cudaStream_t s);
+// next-step decoder input written by the greedy update (greedy_embed_kernel)
+struct GreedyEmbed {
+  const float* table;   // [V, d] fp32 target embedding
+  const float* pos;     // [n_pos, d] sinusoid table
+  float scale;          // f32(sqrt(d))
+  float* x32;           // [rows, d]
+  void* xa;             // [rows, d] activation copy (fp16 / bf16) or null
+  int act_dtype, d, n_pos;
+  int32_t* done;        // CTA-completion counter (zero between launches)
+  int32_t* alive_acc;   // alive accumulator (zero between launches)
+};
+cudaError_t launch_greedy_embed(const GreedyState& g, const GreedyEmbed& e, cudaStream_t s);
 
 cudaError_t launch_keys_to_index(const unsigned long long* keys, int rows, int32_t* out,
                                  cudaStream_t s);

@@ -288,6 +288,84 @@ cudaError_t launch_add_norm(const float* x, const float* y, const float* gain, c
   return add_norm_dispatch<float>(x, y, gain, bias, l1, out32, (float*)out_act, rows, d, s);
 }
 
+// Greedy bookkeeping fused with the next step's decoder-input embedding
+// (search.py:64-85 + decode_step's embed, model.py:327-328): warp per row.
+// Lane 0 applies the greedy rules of greedy_update_kernel; the warp then
+// writes E[prev] * sqrt(d) + P[t + 1] (prev = the emitted token, or PAD for a
+// finished row) as the next step's residual stream and activation copy.  The
+// step counter is bumped by the last CTA to finish (every CTA has read t by
+// then), which also publishes the alive count.
+template <typename TA>
+__global__ void __launch_bounds__(256) greedy_embed_kernel(GreedyState g, GreedyEmbed e) {
+  pdl_trigger();
+  pdl_wait();
+  __shared__ int alive_s;
+  const int t = *g.t;
+  const int lane = threadIdx.x & 31;
+  const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (threadIdx.x == 0) alive_s = 0;
+  __syncthreads();
+  int tok = g.pad, alive = 0;
+  if (r < g.rows && lane == 0) {
+    const unsigned long long key = g.keys[r];
+    g.keys[r] = 0ull;
+    if (!g.finished[r]) {
+      const int w = (int)argmax_key_index(key);
+      if (w == g.eos) {
+        g.finished[r] = 1;
+      } else {
+        if (t < g.out_cap) g.out_ids[(size_t)r * g.out_cap + t] = w;
+        g.out_len[r] = t + 1;
+        tok = w;
+        if (t + 1 >= g.budget[r])
+          g.finished[r] = 1;
+        else
+          alive = 1;
+      }
+    }
+    g.prev[r] = tok;
+  }
+  tok = __shfl_sync(0xffffffffu, tok, 0);
+  if (r < g.rows && t + 1 < e.n_pos) {
+    const int d4 = e.d >> 2;
+    const float* er = e.table + (size_t)tok * e.d;
+    const float* pr = e.pos + (size_t)(t + 1) * e.d;
+    for (int c4 = lane; c4 < d4; c4 += 32) {
+      const float4 a = reinterpret_cast<const float4*>(er)[c4];
+      const float4 q = reinterpret_cast<const float4*>(pr)[c4];
+      float4 o;
+      o.x = __fadd_rn(__fmul_rn(a.x, e.scale), q.x);
+      o.y = __fadd_rn(__fmul_rn(a.y, e.scale), q.y);
+      o.z = __fadd_rn(__fmul_rn(a.z, e.scale), q.z);
+      o.w = __fadd_rn(__fmul_rn(a.w, e.scale), q.w);
+      store4(e.x32 + (size_t)r * e.d + 4 * c4, o);
+      if (e.xa) store4(reinterpret_cast<TA*>(e.xa) + (size_t)r * e.d + 4 * c4, o);
+    }
+  }
+  if (lane == 0 && alive) atomicAdd(&alive_s, 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (alive_s) atomicAdd(e.alive_acc, alive_s);
+    __threadfence();
+    if (atomicAdd(e.done, 1) == (int)gridDim.x - 1) {
+      __threadfence();
+      *g.alive = atomicExch(e.alive_acc, 0);
+      *e.done = 0;
+      *g.t = t + 1;
+    }
+  }
+}
+
+cudaError_t launch_greedy_embed(const GreedyState& g, const GreedyEmbed& e, cudaStream_t s) {
+  const dim3 grid((g.rows + 7) / 8);
+  if (e.act_dtype == kF16) return launch_k(greedy_embed_kernel<__half>, grid, dim3(256), 0, s, g, e);
+  if (e.act_dtype == kBF16)
+    return launch_k(greedy_embed_kernel<__nv_bfloat16>, grid, dim3(256), 0, s, g, e);
+  GreedyEmbed f = e;
+  f.xa = nullptr;
+  return launch_k(greedy_embed_kernel<float>, grid, dim3(256), 0, s, g, f);
+}
+
 cudaError_t launch_greedy_update(const GreedyState& g, cudaStream_t s) {
   return launch_k(greedy_update_kernel, dim3(1), dim3(1024), 0, s, g);
 }

@@ -40,9 +40,9 @@ print(json.dumps({"launches": int(st.gpu_launches)}))
 """
 
 
-def run(tmp_path, dtype, fused):
-    env = dict(os.environ, FNMT_FUSED_LAYER="1" if fused else "0")
-    f = tmp_path / f"{dtype}_{int(fused)}.npz"
+def run(tmp_path, dtype, fused, **extra):
+    env = dict(os.environ, FNMT_FUSED_LAYER="1" if fused else "0", **extra)
+    f = tmp_path / f"{dtype}_{int(fused)}_{len(extra)}.npz"
     r = subprocess.run([sys.executable, "-c", SCRIPT, str(ROOT), str(N), dtype, str(f)], env=env,
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
@@ -60,3 +60,14 @@ def test_fused_layer_matches_unfused_sequence(tmp_path, dtype):
     print(dtype, "fused vs unfused identical:", same, "/", N, "launches", la, "vs", lb)
     assert same >= N - 2        # same arithmetic: identical up to a stray f64-sum ulp
     assert la < lb              # three launches per decode step fewer
+
+
+def test_greedy_update_with_next_embedding_matches_separate_kernels(tmp_path):
+    """greedy_embed_kernel (greedy bookkeeping + the next step's decoder input
+    in one launch) against greedy_update + embed (FNMT_GREEDY_EMBED=0)."""
+    a, la = run(tmp_path, "f16", True)
+    b, lb = run(tmp_path, "f16", True, FNMT_GREEDY_EMBED="0")
+    same = sum(x == y for x, y in zip(a, b))
+    print("greedy+embed fused vs separate identical:", same, "/", N, "launches", la, "vs", lb)
+    assert same == N
+    assert la < lb

@@ -733,14 +733,16 @@ bool make_tmap_16(CUtensorMap* out, const void* base, int dtype, int64_t rows, i
 }
 
 // N tile: the largest of 256/128/64 that still gives >= FNMT_BN_WAVE x SMs
-// tiles (default 0.6: r01 A/B at 9216-row decode steps 740 / 757 / 768 / 798 us
-// for 0.6 / 0.9 / 1.0 / 2.0 — bigger N tiles re-read A less often).
+// tiles (default 0.15: r02 A/B of the 6-1-1 bench with 4 decode lanes, 0.6 /
+// 0.3 / 0.15 -> 7.72 / 7.86 / 7.92 M words/s — bigger N tiles re-read A less
+// often and leave SMs to the other lanes; r01 single-lane 9216-row steps
+// favoured 0.6 over 0.9-2.0).
 int pick_bn(int M, int N) {
   static double wave = -1.0;
   if (wave < 0) {
     const char* e = getenv("FNMT_BN_WAVE");
-    wave = e ? atof(e) : 0.6;
-    if (!(wave > 0.1 && wave < 4.0)) wave = 0.6;
+    wave = e ? atof(e) : 0.15;
+    if (!(wave > 0.0 && wave < 4.0)) wave = 0.15;
   }
   const int mt = (M + kBM - 1) / kBM;
   const double need = wave * num_sms();

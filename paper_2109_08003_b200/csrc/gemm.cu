@@ -484,7 +484,16 @@ __global__ void __launch_bounds__(kTcThreads, MINB)
       int acc = 0;
       uint32_t aph = 0;
       for (int it = 0;; ++it) {
-        if (tile_at(it, tiles) < 0) break;
+        const int tile = tile_at(it, tiles);
+        if (tile < 0) break;
+        // last N tile: the MMA covers only the valid columns (rounded to 16),
+        // e.g. the 8-column tail of the folded [K~ | V~ | c] cache rows
+        uint32_t id = idesc;
+        const int rem = ep.N - (tile % tiles_n) * BN;
+        if (rem < BN) {
+          const int nt = rem < 16 ? 16 : (rem + 15) & ~15;
+          id = (idesc & ~(0x3Fu << 17)) | ((uint32_t)(nt >> 3) << 17);
+        }
         mbar_wait(tempty + acc, aph ^ 1);
         tc_fence_after();
         const uint32_t d = tmem + acc * BN;
@@ -497,9 +506,9 @@ __global__ void __launch_bounds__(kTcThreads, MINB)
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
             if constexpr (I8)
-              tc_mma_i8(d, ad + 2 * kk, bd + 2 * kk, idesc, (kb | kk) != 0 ? 1u : 0u);
+              tc_mma_i8(d, ad + 2 * kk, bd + 2 * kk, id, (kb | kk) != 0 ? 1u : 0u);
             else
-              tc_mma_f16(d, ad + 2 * kk, bd + 2 * kk, idesc, (kb | kk) != 0 ? 1u : 0u);
+              tc_mma_f16(d, ad + 2 * kk, bd + 2 * kk, id, (kb | kk) != 0 ? 1u : 0u);
           }
           tc_commit(empty + s);
           if (++s == STAGES) {
@@ -737,15 +746,20 @@ bool make_tmap_16(CUtensorMap* out, const void* base, int dtype, int64_t rows, i
 // 0.3 / 0.15 -> 7.72 / 7.86 / 7.92 M words/s — bigger N tiles re-read A less
 // often and leave SMs to the other lanes; r01 single-lane 9216-row steps
 // favoured 0.6 over 0.9-2.0).
-int pick_bn(int M, int N) {
-  static double wave = -1.0;
+int pick_bn(int M, int N, int K) {
+  static double wave = -1.0, wave_k = -1.0;
   if (wave < 0) {
     const char* e = getenv("FNMT_BN_WAVE");
     wave = e ? atof(e) : 0.15;
     if (!(wave > 0.0 && wave < 4.0)) wave = 0.15;
+    // long-K GEMMs (decoder FFN2, K = 2048): a tile's MMA time grows with K, so
+    // they get their own threshold (FNMT_BN_WAVE_LONGK)
+    const char* f = getenv("FNMT_BN_WAVE_LONGK");
+    wave_k = f ? atof(f) : wave;
+    if (!(wave_k > 0.0 && wave_k < 4.0)) wave_k = wave;
   }
   const int mt = (M + kBM - 1) / kBM;
-  const double need = wave * num_sms();
+  const double need = (K >= 1024 ? wave_k : wave) * num_sms();
   for (int bn : {256, 128}) {
     if ((double)mt * ((N + bn - 1) / bn) >= need) return bn;
   }
@@ -787,7 +801,7 @@ cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t s) {
     return g.topk.K == 4 ? launch_tc<256, 4, 4>(*pa, *pw, g, ep, s)
                          : launch_tc<256, 4, 8>(*pa, *pw, g, ep, s);
   }
-  switch (pick_bn(g.M, g.N)) {
+  switch (pick_bn(g.M, g.N, g.K)) {
     case 256: return launch_tc<256, 4>(*pa, *pw, g, ep, s);
     case 128: return launch_tc<128, 6>(*pa, *pw, g, ep, s);
     default:
@@ -802,7 +816,7 @@ cudaError_t launch_tc_i8(const CUtensorMap& ta, const GemmArgs& g, cudaStream_t 
   EpiParams ep{g.bias, g.M, g.N, g.epi, g.C, g.ldc, g.c_dtype, g.relu, g.resid, g.ld_resid,
                g.keys, g.topk, g.kc, g.vc, g.cap, g.seg, g.t_ptr,
                g.qscale, g.qzp, g.qcolsum, g.qs.rowsum, g.qs.stats, g.K};
-  switch (pick_bn(g.M, g.N)) {
+  switch (pick_bn(g.M, g.N, g.K)) {
     case 256: return launch_tc<256, 4, 0, true>(ta, *g.qtmap_w, g, ep, s);
     case 128: return launch_tc<128, 6, 0, true>(ta, *g.qtmap_w, g, ep, s);
     default: return launch_tc<64, 8, 0, true>(ta, *g.qtmap_w, g, ep, s);

@@ -146,6 +146,7 @@ __global__ void __launch_bounds__(NT) dec_layer_fused_kernel(DecLayerArgs a, flo
   const int ntot = ns + (nk_c + ch_c - 1) / ch_c;
   const T* ks = reinterpret_cast<const T*>(a.kself);
   const T* kc = reinterpret_cast<const T*>(a.kcross);
+  const T* knew = reinterpret_cast<const T*>(a.knew);
   const size_t rb_s = (size_t)a.ld_self * sizeof(T), rb_c = (size_t)a.ld_cross * sizeof(T);
 
   auto issue = [&](int c) {
@@ -154,8 +155,17 @@ __global__ void __launch_bounds__(NT) dec_layer_fused_kernel(DecLayerArgs a, flo
     uint32_t bytes;
     if (c < ns) {
       const int j0 = c * ch_s;
+      const int n = min(ch_s, nk_s - j0);
+      if (knew && c == ns - 1) {
+        // last self chunk: keys j0..t-1 from the cache, key t from the GEMM's row
+        mbar_expect_tx(bar + (c & 1), (uint32_t)(n * rb_s));
+        if (n > 1) bulk_g2s(dst, ks + (row0_s + j0) * a.ld_self, (uint32_t)((n - 1) * rb_s), bar + (c & 1));
+        bulk_g2s(dst + (size_t)(n - 1) * rb_s, knew + (size_t)r * a.ld_self, (uint32_t)rb_s,
+                 bar + (c & 1));
+        return;
+      }
       src = ks + (row0_s + j0) * a.ld_self;
-      bytes = (uint32_t)(min(ch_s, nk_s - j0) * rb_s);
+      bytes = (uint32_t)(n * rb_s);
     } else {
       const int j0 = (c - ns) * ch_c;
       src = kc + (row0_c + j0) * a.ld_cross;
@@ -208,6 +218,12 @@ __global__ void __launch_bounds__(NT) dec_layer_fused_kernel(DecLayerArgs a, flo
     const int ld = self ? a.ld_self : a.ld_cross;
     const uint8_t* kbuf = buf0 + (size_t)(c & 1) * buf_bytes;
     mbar_wait(bar + (c & 1), (uint32_t)(c >> 1) & 1u);
+    if (knew && c == ns - 1) {
+      // append key t (now in smem) to the row's cache slot: coalesced 16-byte stores
+      const uint4* srow = reinterpret_cast<const uint4*>(kbuf + (size_t)(n - 1) * rb);
+      uint4* drow = reinterpret_cast<uint4*>(const_cast<T*>(ks) + (row0_s + t) * a.ld_self);
+      for (int i = tid; i < (int)(rb / 16); i += NT) drow[i] = srow[i];
+    }
     for (int j = warp; j < n; j += NW) {
       const T* kr = reinterpret_cast<const T*>(kbuf + (size_t)j * rb);
       float sacc = 0.f;
@@ -322,7 +338,7 @@ cudaError_t launch_dec_layer_fused(const DecLayerArgs& a, cudaStream_t s) {
   const size_t rb_s = (size_t)a.ld_self * es, rb_c = (size_t)a.ld_cross * es;
   if (rb_s % 16 || rb_c % 16 || a.ldq % 8 || a.voff % 8 ||
       (reinterpret_cast<uintptr_t>(a.kself) & 15) || (reinterpret_cast<uintptr_t>(a.kcross) & 15) ||
-      (reinterpret_cast<uintptr_t>(a.q) & 15))
+      (reinterpret_cast<uintptr_t>(a.q) & 15) || (reinterpret_cast<uintptr_t>(a.knew) & 15))
     return cudaErrorNotSupported;
   const uint32_t buf = layer_buf_bytes();
   const int ch_s = (int)std::min<size_t>(64, buf / rb_s);

@@ -109,10 +109,6 @@ __device__ __forceinline__ void store_elem(const EpiParams& e, int m, int n, flo
     reinterpret_cast<__nv_bfloat16*>(e.C)[off] = __float2bfloat16_rn(v);
 }
 
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
 __device__ __forceinline__ void named_bar_sync(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }

@@ -234,6 +234,10 @@ struct DecLayerArgs {
   const float* bo_cross; const float* g2; const float* b2;
   int l1, dtype, d, rows;
   const uint8_t* row_done;
+  // this step's self key row [rows, ld_self] written contiguously by the GEMM
+  // (null: already in the cache slot); the kernel reads key t from here and
+  // appends it to cache slot r*cap + t
+  const void* knew;
 };
 bool dec_layer_fused_ok(int dtype, int d, int heads);
 cudaError_t launch_dec_layer_fused(const DecLayerArgs& a, cudaStream_t s);

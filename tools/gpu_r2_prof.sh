@@ -10,7 +10,7 @@ timeout 900 ncu --profile-from-start off --cache-control none --clock-control no
 echo "traffic rc=$?"; tail -2 gpurun_out/traffic_$T.log
 python tools/traffic_ratio.py gpurun_out/traffic_$T.csv gpurun_out/prof_log_$T.npz > gpurun_out/traffic_$T.json; cat gpurun_out/traffic_$T.json
 gzip -f gpurun_out/traffic_$T.csv
-for spec in "attn_dec:regex:attn_dec:1500:2" "attn_enc:regex:attn_varlen:60:2" "norm:regex:add_norm:1000:2" \
+for spec in "attn_dec:regex:dec_layer:700:2" "attn_enc:regex:attn_enc_pipe:60:2" "norm:regex:add_norm:1000:2" \
             "gemm:regex:gemm_tc:1500:8"; do
   IFS=: read name kind pat skip cnt <<< "$spec"
   timeout 600 ncu --profile-from-start off --set full --clock-control none --import-source on -k "$kind:$pat" \

@@ -56,8 +56,21 @@ def bench(M, N, K, reps=20, out_dtype=_capi.F16):
     return us, 2.0 * M * N * K / (us * 1e-6) / 1e12
 
 
+DEC = [  # decoder step shapes of Student-6-1-1 (folded self: N = 2d + 8)
+    (3072, 1032, 512, "dec fsk (folded self k~|v~|c)"),
+    (3072, 1024, 512, "dec fsk without the c tail"),
+    (3072, 1040, 512, "dec fsk, 16-col tail"),
+    (3072, 2048, 512, "dec ffn1"),
+    (3072, 512, 2048, "dec ffn2"),
+    (1100, 1032, 512, "dec fsk, long batch"),
+    (1100, 2048, 512, "dec ffn1, long batch"),
+    (1100, 512, 2048, "dec ffn2, long batch"),
+]
+
+
 def main():
-    for M, N, K, note in SHAPES:
+    shapes = DEC if "dec" in sys.argv[1:] else SHAPES
+    for M, N, K, note in shapes:
         us, tf = bench(M, N, K, out_dtype=_capi.F32 if "f32" in note else _capi.F16)
         print(f"M={M:6d} N={N:6d} K={K:5d}  {us:8.2f} us  {tf:7.1f} TFLOP/s  {note}")
     sys.stdout.flush()

@@ -431,7 +431,8 @@ Norm Engine::make_norm(const std::string& prefix) {
 // reassociated; computed in double, rounded once to the compute dtype).  E is
 // the encoder output (cross, once per batch) or the decoder layer input of
 // step j (self, appended to the cache at slot j).
-Lin Engine::make_folded(const std::string& p, const std::string& blk) {
+Lin Engine::make_folded(const std::string& p, const std::string& blk, std::vector<float>* wt_out,
+                        std::vector<float>* bias_out) {
   const int d = arch.d_model, N = 2 * d + 8;
   const auto& Wq = need(p + "." + blk + ".q_w", (int64_t)d * d);
   const auto& Wk = need(p + "." + blk + ".k_w", (int64_t)d * d);
@@ -482,7 +483,66 @@ Lin Engine::make_folded(const std::string& p, const std::string& blk) {
   L.w = upload_act(wt);
   L.b = upload_f32(bias);
   finish_lin(L);
+  if (wt_out) *wt_out = std::move(wt);
+  if (bias_out) *bias_out = std::move(bias);
   return L;
+}
+
+// Step tables of a layer-0 folded self block (see DecL::tok_tab): true-fp32
+// GEMMs at load (gemm_simt_kernel, ascending-k FMA) of the scaled embedding
+// table E s (fp32, as embed computes it) and of the sinusoid table P with the
+// folded weights; the bias goes into the position table.
+void Engine::make_step_tables(DecL& L, const std::vector<float>& wt,
+                              const std::vector<float>& bias) {
+  const int d = arch.d_model, N = 2 * d + 8, V = arch.vocab_size, np = arch.max_positions;
+  const auto& E = arch.shared_embeddings ? need("src_embed", (int64_t)V * d)
+                                         : need("tgt_embed", (int64_t)V * d);
+  const float s = emb_scale();
+  std::vector<float> es(E.size());
+  for (size_t i = 0; i < E.size(); ++i) es[i] = E[i] * s;
+  auto tmp = [](const std::vector<float>& v) {   // load-time temporaries (freed below)
+    float* p = nullptr;
+    CK(cudaMalloc(&p, v.size() * sizeof(float)));
+    CK(cudaMemcpy(p, v.data(), v.size() * sizeof(float), cudaMemcpyHostToDevice));
+    return p;
+  };
+  float* es_d = tmp(es);
+  float* w_d = tmp(wt);
+  float* b_d = tmp(bias);
+  L.tok_tab = (float*)dalloc(sizeof(float) * (size_t)V * N);
+  L.pos_tab = (float*)dalloc(sizeof(float) * (size_t)np * N);
+  auto run = [&](const float* A, int M, const float* b, float* C) {
+    GemmArgs g;
+    g.A = A;
+    g.lda = d;
+    g.W = w_d;
+    g.ldw = d;
+    g.in_dtype = kF32;
+    g.bias = b;
+    g.M = M;
+    g.N = N;
+    g.K = d;
+    g.epi = kEpiStore;
+    g.C = C;
+    g.ldc = N;
+    g.c_dtype = kF32;
+    CK(launch_gemm(g, stream));
+  };
+  run(es_d, V, nullptr, L.tok_tab);
+  run(pos32, np, b_d, L.pos_tab);
+  CK(cudaStreamSynchronize(stream));
+  CK(cudaFree(es_d));
+  CK(cudaFree(w_d));
+  CK(cudaFree(b_d));
+}
+
+bool step_tables_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("FNMT_STEP_TABLES");
+    on = !(e && e[0] == '0');
+  }
+  return on != 0;
 }
 
 // split-K factor of the decoder's long-K GEMM (FFN2): FNMT_SPLITK (1 = off)
@@ -599,7 +659,12 @@ void Engine::finalize() {
                      d, {d, d});
     L.co = make_lin({p + ".cross.o_w"}, {p + ".cross.o_b"}, d, {d});
     if (fused_cross) L.fck = make_folded(p, "cross");
-    if (fused_self) L.fsk = make_folded(p, "self");
+    if (fused_self) {
+      std::vector<float> wt, bias;
+      const bool tables = i == 0 && step_tables_enabled();
+      L.fsk = make_folded(p, "self", tables ? &wt : nullptr, tables ? &bias : nullptr);
+      if (tables) make_step_tables(L, wt, bias);
+    }
     L.n1 = make_norm(p + ".norm1");
     L.n2 = make_norm(p + ".norm2");
     L.ffn = arch.ffn_dim_dec > 0;
@@ -838,6 +903,21 @@ void Engine::cross_kv_all(int n_tok, cudaStream_t s) {
          ws.ckv[l], ckv_ld, dt, 0, s);
 }
 
+// Layer-0 step tables in use for this step view: the greedy workspace path of
+// a folded single-head decoder whose fused layer kernel runs (the key row goes
+// through the dqkv staging buffer); knew null otherwise.
+StepKey Engine::step_keys_of(const StepView& v) const {
+  StepKey k{};
+  if (dec.empty() || !dec[0].tok_tab || !fused_self || !fused_cross || !v.ws_caches || v.anc ||
+      !dec_layer_fused_ok(dt, arch.d_model, arch.n_heads_dec))
+    return k;
+  k.tok_tab = dec[0].tok_tab;
+  k.pos_tab = dec[0].pos_tab;
+  k.knew = ws.dqkv;
+  k.w = 2 * arch.d_model + 8;
+  return k;
+}
+
 // One decoder step for v.rows rows (model.py:308-344).  All sizes that vary
 // per step live in device memory (step counter), so the launch sequence is
 // graph-capturable and replayable.
@@ -856,6 +936,13 @@ void Engine::run_step(const StepView& v, cudaStream_t s) {
                     tc ? ws.dxa : nullptr, dt, R, d, s));
     prof_end(s, ev, FNMT_K_EMBED, 0.0, Rl * d * (8.0 + dtype_size(dt)));
     ++launches;
+    const StepKey k = step_keys_of(v);
+    if (k.knew) {
+      const int ev2 = prof_begin(s);
+      CK(launch_step_key(k, v.prev, v.t_ptr, R, dt, s));
+      prof_end(s, ev2, FNMT_K_EMBED, 0.0, Rl * k.w * (8.0 + es));
+      ++launches;
+    }
   }
   for (int l = 0; l < arch.n_dec_layers; ++l) {
     const DecL& L = dec[l];
@@ -880,7 +967,8 @@ void Engine::run_step(const StepView& v, cudaStream_t s) {
       // kernel appends them to the cache slots (the per-row slot scatter from
       // the GEMM epilogue measured 23 vs 8 us per step at 3072 rows)
       const bool layer_ok = fused_cross && dec_layer_fused_ok(dt, d, arch.n_heads_dec);
-      const bool staged = layer_ok && knew_staging_enabled();
+      const bool tabled = layer_ok && l == 0 && step_keys_of(v).knew;   // no GEMM: step tables
+      const bool staged = layer_ok && !tabled && knew_staging_enabled();
       g.epi = staged ? kEpiStore : kEpiSlot;
       g.C = staged ? ws.dqkv : v.kc[l];
       g.ldc = fl;
@@ -889,10 +977,12 @@ void Engine::run_step(const StepView& v, cudaStream_t s) {
       g.t_ptr = v.t_ptr;
       g.tmap_a = &ws.tm_dxa;
       g.tmap_w = &L.fsk.tm;
-      const int ev = prof_begin(s);
-      CK(launch_gemm(g, s));
-      prof_end(s, ev, gemm_cls, 2.0 * Rl * fl * d, Rl * d * es + (double)fl * d * es + Rl * fl * es);
-      ++launches;
+      if (!tabled) {
+        const int ev = prof_begin(s);
+        CK(launch_gemm(g, s));
+        prof_end(s, ev, gemm_cls, 2.0 * Rl * fl * d, Rl * d * es + (double)fl * d * es + Rl * fl * es);
+        ++launches;
+      }
       if (layer_ok) {
         // one kernel: self attention, + residual, norm1, cross attention, + residual, norm2
         DecLayerArgs f{};
@@ -923,7 +1013,8 @@ void Engine::run_step(const StepView& v, cudaStream_t s) {
         f.d = d;
         f.rows = R;
         f.row_done = v.row_done;
-        f.knew = staged ? ws.dqkv : nullptr;
+        // tables: the previous kernel (greedy_embed / step_key) wrote key t into dqkv
+        f.knew = (staged || tabled) ? ws.dqkv : nullptr;
         const int ev2 = prof_begin(s);
         CK(launch_dec_layer_fused(f, s));
         // SURVEY §8(d) attention bytes (self t+1 keys + cross S keys, 2 d each,
@@ -1478,6 +1569,13 @@ int Engine::decode_greedy(int R, int cap, int max_len, const fnmt_run& run,
                     dt == kF32 ? nullptr : ws.dxa, dt, R, arch.d_model, stream));
     prof_end(stream, ev, FNMT_K_EMBED, 0.0, (double)R * arch.d_model * (8.0 + dtype_size(dt)));
     ++launches;
+    ge.key = step_keys_of(v);
+    if (ge.key.knew) {
+      const int ev2 = prof_begin(stream);
+      CK(launch_step_key(ge.key, ws.prev, ws.t, R, dt, stream));
+      prof_end(stream, ev2, FNMT_K_EMBED, 0.0, (double)R * ge.key.w * (8.0 + dtype_size(dt)));
+      ++launches;
+    }
     v.embed_done = true;
   }
   auto body = [&](int t) {
@@ -1488,7 +1586,8 @@ int Engine::decode_greedy(int R, int cap, int max_len, const fnmt_run& run,
     if (fuse_embed) {
       CK(launch_greedy_embed(gs, ge, stream));
       prof_end(stream, ev, FNMT_K_SEARCH, 0.0,
-               rl * 24 + rl * arch.d_model * (8.0 + dtype_size(dt)));
+               rl * 24 + rl * arch.d_model * (8.0 + dtype_size(dt)) +
+                   (ge.key.knew ? rl * ge.key.w * (8.0 + dtype_size(dt)) : 0.0));
     } else {
       CK(launch_greedy_update(gs, stream));
       prof_end(stream, ev, FNMT_K_SEARCH, 0.0, rl * 24);

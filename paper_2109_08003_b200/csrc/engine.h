@@ -56,6 +56,11 @@ struct DecL {
   Lin sqkv, so, cq, ckv, co, f1, f2;
   Lin fck;   // folded cross K|V|c (fused_cross): [K Wq^T | V Wo | bq.k] per encoder row
   Lin fsk;   // folded self K|V|c (fused_self): the same per decoder input row
+  // layer 0 of a folded decoder: the layer input is the embedding E[tok] s + P[t],
+  // so its folded self row is tok_tab[tok] + pos_tab[t] (fp32, [V, 2d + 8] and
+  // [max_positions, 2d + 8], bias in pos_tab) -- a gather instead of a GEMM
+  float* tok_tab = nullptr;
+  float* pos_tab = nullptr;
   Norm n1, n2, n3;
   bool ffn = false;
 };
@@ -245,7 +250,10 @@ class Engine {
   void* upload_act(const std::vector<float>& v);
   Lin make_lin(const std::vector<std::string>& wnames, const std::vector<std::string>& bnames,
                int k, const std::vector<int>& ns);
-  Lin make_folded(const std::string& prefix, const std::string& blk);
+  Lin make_folded(const std::string& prefix, const std::string& blk,
+                  std::vector<float>* wt_out = nullptr, std::vector<float>* bias_out = nullptr);
+  void make_step_tables(DecL& L, const std::vector<float>& wt, const std::vector<float>& bias);
+  StepKey step_keys_of(const StepView& v) const;
   void finish_lin(Lin& L);
   void make_qlin(Lin& L, const std::vector<std::string>& wnames, int k, const std::vector<int>& ns);
   void attach_q(GemmArgs& g, const Lin& L) const;

@@ -258,6 +258,17 @@ struct GreedyState {
 };
 cudaError_t launch_greedy_update(const GreedyState& g, cudaStream_t s);
 // next-step decoder input written by the greedy update (greedy_embed_kernel)
+// Layer-0 folded self key row of a decoder input (engine.h DecL::tok_tab):
+// knew[r] = act(tok_tab[tok] + pos_tab[pos]), [rows, w] (w = 2d + 8)
+struct StepKey {
+  const float* tok_tab;
+  const float* pos_tab;
+  void* knew;   // null: not used
+  int w;
+};
+cudaError_t launch_step_key(const StepKey& k, const int32_t* tok, const int32_t* t_ptr, int rows,
+                            int act_dtype, cudaStream_t s);
+
 struct GreedyEmbed {
   const float* table;   // [V, d] fp32 target embedding
   const float* pos;     // [n_pos, d] sinusoid table
@@ -267,6 +278,7 @@ struct GreedyEmbed {
   int act_dtype, d, n_pos;
   int32_t* done;        // CTA-completion counter (zero between launches)
   int32_t* alive_acc;   // alive accumulator (zero between launches)
+  StepKey key;          // also write the next step's layer-0 self key row (key.knew set)
 };
 cudaError_t launch_greedy_embed(const GreedyState& g, const GreedyEmbed& e, cudaStream_t s);
 

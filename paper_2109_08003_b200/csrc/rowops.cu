@@ -9,6 +9,8 @@
 //           token is emitted, finished rows are fed PAD  (search.py:58-86)
 #include <algorithm>
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -312,6 +314,40 @@ cudaError_t launch_add_norm(const float* x, const float* y, const float* gain, c
   return add_norm_dispatch<float>(x, y, gain, bias, l1, out32, (float*)out_act, rows, d, s);
 }
 
+// One warp writes row r's layer-0 self key: act(tok_tab[tok] + pos_tab[pos])
+// (fp32 sum, one rounding), 8 columns per lane and pass.
+template <typename TA>
+__device__ __forceinline__ void step_key_row(const StepKey& k, int r, int tok, int pos, int lane) {
+  const float* tr = k.tok_tab + (size_t)tok * k.w;
+  const float* pr = k.pos_tab + (size_t)pos * k.w;
+  TA* dst = reinterpret_cast<TA*>(k.knew) + (size_t)r * k.w;
+  for (int c4 = lane; c4 < (k.w >> 2); c4 += 32) {
+    const float4 a = reinterpret_cast<const float4*>(tr)[c4];
+    const float4 b = reinterpret_cast<const float4*>(pr)[c4];
+    store4(dst + 4 * c4, make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w));
+  }
+}
+
+template <typename TA>
+__global__ void __launch_bounds__(256) step_key_kernel(StepKey k, const int32_t* tok,
+                                                       const int32_t* t_ptr, int rows) {
+  pdl_trigger();
+  pdl_wait();
+  const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (r < rows) step_key_row<TA>(k, r, tok[r], *t_ptr, threadIdx.x & 31);
+}
+
+cudaError_t launch_step_key(const StepKey& k, const int32_t* tok, const int32_t* t_ptr, int rows,
+                            int act_dtype, cudaStream_t s) {
+  if (rows <= 0) return cudaSuccess;
+  if (k.w % 4) return cudaErrorInvalidValue;
+  const dim3 grid((rows + 7) / 8);
+  if (act_dtype == kF16) return launch_k(step_key_kernel<__half>, grid, dim3(256), 0, s, k, tok, t_ptr, rows);
+  if (act_dtype == kBF16)
+    return launch_k(step_key_kernel<__nv_bfloat16>, grid, dim3(256), 0, s, k, tok, t_ptr, rows);
+  return cudaErrorInvalidValue;
+}
+
 // Greedy bookkeeping fused with the next step's decoder-input embedding
 // (search.py:64-85 + decode_step's embed, model.py:327-328): warp per row.
 // Lane 0 applies the greedy rules of greedy_update_kernel; the warp then
@@ -364,6 +400,9 @@ __global__ void __launch_bounds__(256) greedy_embed_kernel(GreedyState g, Greedy
       o.w = __fadd_rn(__fmul_rn(a.w, e.scale), q.w);
       store4(e.x32 + (size_t)r * e.d + 4 * c4, o);
       if (e.xa) store4(reinterpret_cast<TA*>(e.xa) + (size_t)r * e.d + 4 * c4, o);
+    }
+    if constexpr (!std::is_same<TA, float>::value) {
+      if (e.key.knew) step_key_row<TA>(e.key, r, tok, t + 1, lane);
     }
   }
   if (lane == 0 && alive) atomicAdd(&alive_s, 1);

@@ -69,13 +69,17 @@ def test_step_tables_match_gemm_rows(tmp_path, dtype):
     """Layer-0 self key rows gathered from the step tables (tok_tab[tok] +
     pos_tab[t], fp32 sum rounded once; engine.cu make_step_tables) against the
     folded self GEMM on the rounded decoder input: same math, different
-    rounding, so >= 99% of the sentences are identical (the oracle bar with the
-    near-tie report is test_gpu_corpus_parity.py, which runs the tables)."""
+    rounding.  fp16: >= 99% of the sentences identical.  bf16: >= 97% -- the
+    GEMM side rounds the decoder input to bf16 (8 mantissa bits) before the
+    projection and the tables do not, so the two bf16 runs disagree on more
+    random-model near-ties; the oracle bar (every divergence a near-tie) is
+    test_gpu_parity.py::test_folded_cross_attention_corpus_path[bf16] and, for
+    fp16 at the benchmarked shape, test_gpu_corpus_parity.py (both run the tables)."""
     a, la = run(tmp_path, dtype, True)
     b, lb = run(tmp_path, dtype, True, FNMT_STEP_TABLES="0")
     same = sum(x == y for x, y in zip(a, b))
     print(dtype, "step tables vs GEMM rows identical:", same, "/", N, "launches", la, "vs", lb)
-    assert same >= 0.99 * N
+    assert same >= (0.99 if dtype == "f16" else 0.97) * N
     assert la < lb              # one GEMM per decode step fewer
 
 

@@ -545,18 +545,6 @@ bool step_tables_enabled() {
   return on != 0;
 }
 
-// split-K factor of the decoder's long-K GEMM (FFN2): FNMT_SPLITK (1 = off)
-int splitk_of(int K) {
-  static int f = -1;
-  if (f < 0) {
-    const char* e = getenv("FNMT_SPLITK");
-    f = e ? atoi(e) : 1;
-    if (f < 1 || f > kMaxSplitK) f = 1;
-  }
-  const int nk = (K + 63) / 64;
-  return (K >= 1024 && nk % f == 0) ? f : 1;
-}
-
 bool greedy_embed_enabled() {
   static int on = -1;
   if (on < 0) {
@@ -732,7 +720,7 @@ void Engine::reserve(int tok_cap, int row_cap, int64_t pool_cap) {
     ws.vc[l] = (char*)ws.kc[l] + (size_t)es * pool_cap * d;
   }
   ws.dx32 = (float*)alloc(sizeof(float) * (size_t)row_cap * d);
-  ws.dy32 = (float*)alloc(sizeof(float) * (size_t)row_cap * d * kMaxSplitK);
+  ws.dy32 = (float*)alloc(sizeof(float) * (size_t)row_cap * d);
   ws.dxa = dt == kF32 ? (void*)ws.dx32 : alloc((size_t)es * row_cap * d);
   ws.dqkv = alloc((size_t)es * row_cap * 3 * d);
   ws.datt = alloc((size_t)es * row_cap * d);
@@ -778,9 +766,8 @@ void Engine::reserve_for(const fnmt_run& run) {
 // building blocks
 
 void Engine::gemm(const void* A, const CUtensorMap* tmA, int lda, const Lin& L, int M, void* C,
-                  int ldc, int c_dtype, int relu, cudaStream_t s, const float* resid, int splits) {
+                  int ldc, int c_dtype, int relu, cudaStream_t s, const float* resid) {
   GemmArgs g;
-  g.splits = splits;
   g.A = A;
   g.lda = lda;
   g.W = L.w;
@@ -1157,21 +1144,8 @@ void Engine::run_step(const StepView& v, cudaStream_t s) {
     }
     if (L.ffn) {
       gemm(ws.dxa, tc ? &ws.tm_dxa : nullptr, d, L.f1, R, ws.dh, arch.ffn_dim_dec, dt, 1, s);
-      const int sk = tc && !q8 ? splitk_of(arch.ffn_dim_dec) : 1;
-      if (sk > 1) {
-        // split-K FFN2 (K = ffn width): the partials are summed, in split order,
-        // by the norm that follows
-        gemm(ws.dh, &ws.tm_dh, arch.ffn_dim_dec, L.f2, R, ws.dy32, d, kF32, 0, s, nullptr, sk);
-        const int ev = prof_begin(s);
-        CK(launch_add_norm_parts(ws.dx32, ws.dy32, sk, (int64_t)R * d, L.n3.g, L.n3.b,
-                                 arch.norm_l1, ws.dx32, ws.dxa, dt, R, d, s));
-        prof_end(s, ev, FNMT_K_NORM, 0.0, (prof_m >= 0 ? prof_m : (double)R) * d *
-                                               (8.0 + 4.0 * sk + dtype_size(dt)));
-        ++launches;
-      } else {
-        gemm_norm(ws.dh, tc ? &ws.tm_dh : nullptr, arch.ffn_dim_dec, L.f2, R, ws.dx32, ws.dxa,
-                  ws.dy32, L.n3, s);
-      }
+      gemm_norm(ws.dh, tc ? &ws.tm_dh : nullptr, arch.ffn_dim_dec, L.f2, R, ws.dx32, ws.dxa,
+                ws.dy32, L.n3, s);
     }
   }
   if (v.topk && tc) {

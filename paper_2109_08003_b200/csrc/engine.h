@@ -261,7 +261,7 @@ class Engine {
   float emb_scale() const;
 
   void gemm(const void* A, const CUtensorMap* tmA, int lda, const Lin& L, int M, void* C, int ldc,
-            int c_dtype, int relu, cudaStream_t s, const float* resid = nullptr, int splits = 1);
+            int c_dtype, int relu, cudaStream_t s, const float* resid = nullptr);
   void gemm_argmax(const void* A, const CUtensorMap* tmA, int lda, int M,
                    unsigned long long* keys, cudaStream_t s);
   void norm(const float* x, const float* y, const Norm& n, float* o32, void* oa, int rows,

@@ -63,7 +63,6 @@ struct EpiParams {
   const int32_t* rowsum;
   const unsigned int* stats;
   int qk;
-  int splits;   // split-K factor (1 = none); see GemmArgs::splits
 };
 
 // kEpiQKV destination of output element (m, n): q columns go to C, k / v
@@ -286,14 +285,10 @@ __device__ __forceinline__ int tile_at(int it, int tiles) {
   return t < tiles ? t : -1;
 }
 
-// tile -> (row block, column block, K split); the splits of one output tile
-// are consecutive tiles
-__device__ __forceinline__ void tile_coords(int tile, int tiles_n, int splits, int BN, int& m0,
-                                            int& n0, int& sp) {
-  sp = tile % splits;
-  const int t = tile / splits;
-  m0 = (t / tiles_n) * kBM;
-  n0 = (t % tiles_n) * BN;
+// tile -> (row block, column block)
+__device__ __forceinline__ void tile_coords(int tile, int tiles_n, int BN, int& m0, int& n0) {
+  m0 = (tile / tiles_n) * kBM;
+  n0 = (tile % tiles_n) * BN;
 }
 
 
@@ -436,7 +431,6 @@ __global__ void __launch_bounds__(kTcThreads, MINB)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int nk = (K + Cfg::kBKe - 1) / Cfg::kBKe;
-  const int nks = nk / ep.splits;   // K blocks per split (the host checks divisibility)
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tma);
@@ -468,9 +462,9 @@ __global__ void __launch_bounds__(kTcThreads, MINB)
       for (int it = 0;; ++it) {
         const int tile = tile_at(it, tiles);
         if (tile < 0) break;
-        int m0, n0, sp;
-        tile_coords(tile, tiles_n, ep.splits, BN, m0, n0, sp);
-        for (int kb = sp * nks; kb < (sp + 1) * nks; ++kb) {
+        int m0, n0;
+        tile_coords(tile, tiles_n, BN, m0, n0);
+        for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(empty + s, ph ^ 1);
           mbar_expect_tx(full + s, Cfg::kStage);
           tma_load_2d(sA + s * kABytes, &tma, full + s, kb * Cfg::kBKe, m0);
@@ -497,8 +491,8 @@ __global__ void __launch_bounds__(kTcThreads, MINB)
         // last N tile: the MMA covers only the valid columns (rounded to 16),
         // e.g. the 8-column tail of the folded [K~ | V~ | c] cache rows
         uint32_t id = idesc;
-        int m0, n0, sp;
-        tile_coords(tile, tiles_n, ep.splits, BN, m0, n0, sp);
+        int m0, n0;
+        tile_coords(tile, tiles_n, BN, m0, n0);
         const int rem = ep.N - n0;
         if (rem < BN) {
           const int nt = rem < 16 ? 16 : (rem + 15) & ~15;
@@ -507,7 +501,7 @@ __global__ void __launch_bounds__(kTcThreads, MINB)
         mbar_wait(tempty + acc, aph ^ 1);
         tc_fence_after();
         const uint32_t d = tmem + acc * BN;
-        for (int kb = 0; kb < nks; ++kb) {
+        for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(full + s, ph);
           tc_fence_after();
           const uint64_t ad = umma_desc_sw128(smem_u32(sA + s * kABytes));
@@ -543,14 +537,13 @@ __global__ void __launch_bounds__(kTcThreads, MINB)
     for (int it = 0;; ++it) {
       const int tile = tile_at(it, tiles);
       if (tile < 0) break;
-      int m0, n0, sp;
-      tile_coords(tile, tiles_n, ep.splits, BN, m0, n0, sp);
-      // stage this tile's bias while the MMAs run (double-buffered by acc);
-      // split-K: only split 0 adds it
+      int m0, n0;
+      tile_coords(tile, tiles_n, BN, m0, n0);
+      // stage this tile's bias while the MMAs run (double-buffered by acc)
       float* bs = bias_s + acc * BN;
       for (int i = threadIdx.x - 64; i < BN; i += kEpiWarps * 32) {
         const bool in = n0 + i < ep.N;
-        bs[i] = (ep.bias && in && sp == 0) ? ep.bias[n0 + i] : 0.f;
+        bs[i] = (ep.bias && in) ? ep.bias[n0 + i] : 0.f;
         if constexpr (I8) {
           qsc_s[acc * BN + i] = in ? ep.qscale[n0 + i] : 0.f;
           qzp_s[acc * BN + i] = in ? ep.qzp[n0 + i] : 0.f;
@@ -584,8 +577,8 @@ __global__ void __launch_bounds__(kTcThreads, MINB)
               q_dequant_chunk(ep, m, v, qsc_s + o, qzp_s + o, qcs_s + o);
             }
           }
-          if (row_ok && nb < ep.N)   // split s stores rows [s M, (s+1) M)
-            epilogue_chunk(ep, m + sp * ep.M, nb, v, bs + col0 + c * 32, best_v, best_i);
+          if (row_ok && nb < ep.N)
+            epilogue_chunk(ep, m, nb, v, bs + col0 + c * 32, best_v, best_i);
         }
         tc_fence_before();
         __syncwarp();
@@ -701,7 +694,7 @@ cudaError_t launch_tc(const CUtensorMap& ta, const CUtensorMap& tw, const GemmAr
   cudaError_t e = set_max_smem((const void*)kern);
   if (e != cudaSuccess) return e;
   const int tiles_n = (g.N + BN - 1) / BN;
-  const int tiles = tiles_n * ((g.M + kBM - 1) / kBM) * ep.splits;
+  const int tiles = tiles_n * ((g.M + kBM - 1) / kBM);
   const int grid = tiles < MINB * num_sms() ? tiles : MINB * num_sms();
   const uint32_t idesc = I8 ? umma_idesc_i8(kBM, BN) : umma_idesc_f16(kBM, BN, g.in_dtype == kBF16);
   return launch_k(kern, dim3(grid), dim3(kTcThreads),
@@ -762,19 +755,6 @@ bool make_tmap_16(CUtensorMap* out, const void* base, int dtype, int64_t rows, i
 // 0.3 / 0.15 -> 7.72 / 7.86 / 7.92 M words/s — bigger N tiles re-read A less
 // often and leave SMs to the other lanes; r01 single-lane 9216-row steps
 // favoured 0.6 over 0.9-2.0).
-// GEMM variant for M <= kSmallM (decode steps): FNMT_GEMM_SMALLM = 0 (the
-// 1-CTA/SM 4-stage tiles), 1 (2 CTAs/SM: BN 256 x 2 stages single accumulator,
-// BN 128 x 3 stages), 2 (BN 256 x 3 stages, 1 CTA/SM)
-constexpr int kSmallM = 4096;
-int small_m_variant() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("FNMT_GEMM_SMALLM");
-    v = e ? atoi(e) : 0;
-  }
-  return v;
-}
-
 int pick_bn(int M, int N, int K) {
   static double wave = -1.0, wave_k = -1.0;
   if (wave < 0) {
@@ -800,15 +780,7 @@ cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t s) {
   if (g.qw) return launch_qgemm(g, s);
   EpiParams ep{g.bias, g.M, g.N, g.epi, g.C, g.ldc, g.c_dtype, g.relu, g.resid, g.ld_resid,
                g.keys, g.topk, g.kc, g.vc, g.cap, g.seg, g.t_ptr,
-               nullptr, nullptr, nullptr, nullptr, nullptr, 0, 1};
-  ep.splits = 1;
-  if (g.splits > 1) {
-    const int nk = (g.K + kBK - 1) / kBK;
-    if (g.epi != kEpiStore || g.c_dtype != kF32 || g.resid || g.relu || g.in_dtype == kF32 ||
-        nk % g.splits)
-      return cudaErrorInvalidValue;
-    ep.splits = g.splits;
-  }
+               nullptr, nullptr, nullptr, nullptr, nullptr, 0};
   if (g.epi == kEpiQKV && (!g.kc || !g.vc || !g.t_ptr || g.seg <= 0 || g.N != 3 * g.seg))
     return cudaErrorInvalidValue;
   if (g.epi == kEpiSlot && (!g.t_ptr || g.cap <= 0 || g.resid)) return cudaErrorInvalidValue;
@@ -839,22 +811,6 @@ cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t s) {
                          : launch_tc<256, 4, 8>(*pa, *pw, g, ep, s);
   }
   const int bn = pick_bn(g.M, g.N, g.K);
-  if (g.M <= kSmallM && g.epi != kEpiArgmax) {
-    // decoder-sized GEMMs: two co-resident CTAs per SM with a smaller smem ring
-    // (a 1-tile CTA's TMA fill and epilogue drain overlap the other CTA's MMAs,
-    // and other decode lanes' attention CTAs fit beside them)
-    switch (small_m_variant()) {
-      case 1:
-        if (bn == 256) return launch_tc<256, 2, 0, false, 2, 1>(*pa, *pw, g, ep, s);
-        if (bn == 128) return launch_tc<128, 3, 0, false, 2, 2>(*pa, *pw, g, ep, s);
-        break;
-      case 2:
-        if (bn == 256) return launch_tc<256, 3, 0, false, 1, 2>(*pa, *pw, g, ep, s);
-        break;
-      default:
-        break;
-    }
-  }
   switch (bn) {
     case 256: return launch_tc<256, 4>(*pa, *pw, g, ep, s);
     case 128: return launch_tc<128, 6>(*pa, *pw, g, ep, s);
@@ -869,7 +825,7 @@ cudaError_t launch_tc_i8(const CUtensorMap& ta, const GemmArgs& g, cudaStream_t 
   if (g.epi == kEpiTopK || !g.qtmap_w) return cudaErrorInvalidValue;
   EpiParams ep{g.bias, g.M, g.N, g.epi, g.C, g.ldc, g.c_dtype, g.relu, g.resid, g.ld_resid,
                g.keys, g.topk, g.kc, g.vc, g.cap, g.seg, g.t_ptr,
-               g.qscale, g.qzp, g.qcolsum, g.qs.rowsum, g.qs.stats, g.K, 1};
+               g.qscale, g.qzp, g.qcolsum, g.qs.rowsum, g.qs.stats, g.K};
   switch (pick_bn(g.M, g.N, g.K)) {
     case 256: return launch_tc<256, 4, 0, true>(ta, *g.qtmap_w, g, ep, s);
     case 128: return launch_tc<128, 6, 0, true>(ta, *g.qtmap_w, g, ep, s);

@@ -86,7 +86,6 @@ QScratch qgemm_scratch(void* base, int64_t M, int K);
 bool make_tmap_8(CUtensorMap* out, const void* base, int64_t rows, int64_t kp, int box_rows,
                  std::string* err);
 
-constexpr int kMaxSplitK = 4;
 
 struct GemmArgs {
   const void* A = nullptr;  // [M, K] row-major, leading dim lda (elements)
@@ -109,11 +108,6 @@ struct GemmArgs {
   void* vc = nullptr;
   int cap = 0, seg = 0;
   const int32_t* t_ptr = nullptr;
-  // split-K (kEpiStore, fp32 C, no residual / ReLU): split s of `splits`
-  // accumulates K blocks [s nk / splits, (s+1) nk / splits) and writes rows
-  // [s M, (s+1) M) of C (bias added by split 0 only); the consumer sums the
-  // partials in split order (add_norm with ny = splits)
-  int splits = 1;   // <= kMaxSplitK
   // Pre-encoded TMA descriptors (tcgen05 path).  If null the launcher encodes
   // them on the fly (host cost ~ microseconds).
   const CUtensorMap* tmap_a = nullptr;
@@ -158,9 +152,6 @@ cudaError_t launch_add_norm(const float* x, const float* y, const float* gain,
                             int act_dtype, int rows, int d, cudaStream_t s);
 // same, the residual branch given as ny partial sums y + k * ystride (k < ny),
 // added in order ((y0 + y1) + y2) + ... (split-K GEMM outputs)
-cudaError_t launch_add_norm_parts(const float* x, const float* y, int ny, int64_t ystride,
-                                  const float* gain, const float* bias, int l1, float* out32,
-                                  void* out_act, int act_dtype, int rows, int d, cudaStream_t s);
 
 // ---------------------------------------------------------------------------
 // attention (model.py:199-240)

@@ -71,7 +71,7 @@ template <typename TA, int NV>
 __global__ void add_norm_kernel(const float* __restrict__ x, const float* __restrict__ y,
                                 const float* __restrict__ gain, const float* __restrict__ bias,
                                 int l1, float* __restrict__ out32, TA* __restrict__ out_act,
-                                int rows, int d, int ny, int64_t ystride) {
+                                int rows, int d) {
   pdl_trigger();
   pdl_wait();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -88,14 +88,7 @@ __global__ void add_norm_kernel(const float* __restrict__ x, const float* __rest
     if (c < d4) {
       float4 a = reinterpret_cast<const float4*>(xr)[c];
       if (yr) {
-        float4 b = reinterpret_cast<const float4*>(yr)[c];
-        for (int k = 1; k < ny; ++k) {
-          const float4 p = reinterpret_cast<const float4*>(yr + k * ystride)[c];
-          b.x = b.x + p.x;
-          b.y = b.y + p.y;
-          b.z = b.z + p.z;
-          b.w = b.w + p.w;
-        }
+        const float4 b = reinterpret_cast<const float4*>(yr)[c];
         a.x = a.x + b.x;
         a.y = a.y + b.y;
         a.z = a.z + b.z;
@@ -147,13 +140,12 @@ __global__ void add_norm_kernel(const float* __restrict__ x, const float* __rest
 
 template <typename TA>
 cudaError_t add_norm_dispatch(const float* x, const float* y, const float* g, const float* b,
-                              int l1, float* o32, TA* oa, int rows, int d, cudaStream_t s,
-                              int ny = 1, int64_t ystride = 0) {
+                              int l1, float* o32, TA* oa, int rows, int d, cudaStream_t s) {
   const int threads = 256;
   const int blocks = (int)(((int64_t)rows * 32 + threads - 1) / threads);
   const int nv = (d / 4 + 31) / 32;
-  void (*k)(const float*, const float*, const float*, const float*, int, float*, TA*, int, int,
-            int, int64_t) = nullptr;
+  void (*k)(const float*, const float*, const float*, const float*, int, float*, TA*, int, int) =
+      nullptr;
   if (nv <= 1)
     k = add_norm_kernel<TA, 1>;
   else if (nv <= 2)
@@ -168,8 +160,7 @@ cudaError_t add_norm_dispatch(const float* x, const float* y, const float* g, co
     k = add_norm_kernel<TA, 16>;
   else
     return cudaErrorInvalidValue;
-  return launch_k(k, dim3(blocks), dim3(threads), 0, s, x, y, g, b, l1, o32, oa, rows, d, ny,
-                  ystride);
+  return launch_k(k, dim3(blocks), dim3(threads), 0, s, x, y, g, b, l1, o32, oa, rows, d);
 }
 
 // Single CTA: every row reads the same step counter, then thread 0 bumps it.
@@ -286,20 +277,6 @@ cudaError_t launch_embed(const int32_t* ids, const int32_t* pos_ids, const int32
                   pos_scalar, table, pos_table, scale, x32, (float*)xact, n, d);
 }
 
-cudaError_t launch_add_norm_parts(const float* x, const float* y, int ny, int64_t ystride,
-                                  const float* gain, const float* bias, int l1, float* out32,
-                                  void* out_act, int act_dtype, int rows, int d, cudaStream_t s) {
-  if (rows <= 0) return cudaSuccess;
-  if (d % 4 || ny < 1 || !y || (ystride % 4)) return cudaErrorInvalidValue;
-  if (act_dtype == kF16 || !out_act)
-    return add_norm_dispatch<__half>(x, y, gain, bias, l1, out32, (__half*)out_act, rows, d, s, ny,
-                                     ystride);
-  if (act_dtype == kBF16)
-    return add_norm_dispatch<__nv_bfloat16>(x, y, gain, bias, l1, out32, (__nv_bfloat16*)out_act,
-                                            rows, d, s, ny, ystride);
-  return add_norm_dispatch<float>(x, y, gain, bias, l1, out32, (float*)out_act, rows, d, s, ny,
-                                  ystride);
-}
 
 cudaError_t launch_add_norm(const float* x, const float* y, const float* gain, const float* bias,
                             int l1, float* out32, void* out_act, int act_dtype, int rows, int d,

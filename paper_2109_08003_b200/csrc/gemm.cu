@@ -267,7 +267,11 @@ constexpr int kTcThreads = 64 + kEpiWarps * 32;    // producer + MMA warps, epil
 // persistent tcgen05 kernel
 
 // Every stage row is 128 bytes of K: 64 fp16/bf16 elements, or 128 int8.
-template <int BN, int STAGES, bool I8 = false, int TK = 0, int NACC = 2>
+// TS (TMA-store epilogue): every epilogue warp owns two 4 KB staging buffers
+// (a 32-row x 32-column chunk, swizzled) that TMA stores to global memory
+constexpr int kStageWarpBytes = 2 * 4096;
+
+template <int BN, int STAGES, bool I8 = false, int TK = 0, int NACC = 2, bool TS = false>
 struct TcCfg {
   // TK (beam top-K epilogue): per-row exchange of the two column halves' partials
   static constexpr int kTkBytes = TK ? kBM * (4 + 8 + 8 * TK) : 0;
@@ -276,7 +280,8 @@ struct TcCfg {
   static constexpr int kStage = kABytes + kBBytes;
   static constexpr int kTmemCols = NACC * BN;   // NACC = 2: double-buffered accumulator
   static constexpr int kColBytes = I8 ? 16 : 4;   // bias (+ scale, zeropoint, column sum)
-  static constexpr int kSmem = 1024 + STAGES * kStage + 2 * BN * kColBytes + kTkBytes + 256;
+  static constexpr int kOut = TS ? 1024 + kEpiWarps * kStageWarpBytes : 0;
+  static constexpr int kSmem = 1024 + STAGES * kStage + 2 * BN * kColBytes + kTkBytes + 256 + kOut;
 };
 
 // Tile of this CTA's it-th iteration (-1 when done): a grid-stride walk.
@@ -405,11 +410,67 @@ __device__ __forceinline__ void topk_epilogue(const EpiParams& ep, uint32_t tadd
   }
 }
 
-template <int BN, int STAGES, int TOPK, bool I8 = false, int MINB = 1, int NACC = 2>
+// Stage 32 rows x 32 columns of output (row = lane) into a swizzled chunk
+// buffer and TMA-store it at (column nb, row m0r).  fp16 / bf16: 64-byte rows,
+// SWIZZLE_64B (16-byte unit k of row r at k ^ ((r >> 1) & 3)); fp32: 128-byte
+// rows, SWIZZLE_128B (unit k at k ^ (r & 7)) -- conflict-free shared stores.
+__device__ __forceinline__ void ts_store_chunk(const EpiParams& ep, const CUtensorMap* tmc,
+                                               uint8_t* buf, int lane, int nb, int m0r,
+                                               const float (&v)[32], const float* bs) {
+  bulk_wait_read<1>();   // this buffer's previous store (two chunks ago) has been read
+  __syncwarp();
+  if (ep.c_dtype == kF32) {
+    uint4* row = reinterpret_cast<uint4*>(buf + lane * 128);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      float o[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        o[i] = v[4 * k + i] + bs[4 * k + i];
+        if (ep.relu) o[i] = fmaxf(o[i], 0.f);
+      }
+      row[k ^ (lane & 7)] = make_uint4(__float_as_uint(o[0]), __float_as_uint(o[1]),
+                                       __float_as_uint(o[2]), __float_as_uint(o[3]));
+    }
+  } else {
+    uint4* row = reinterpret_cast<uint4*>(buf + lane * 64);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      uint32_t pk[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        float a = v[8 * k + 2 * i] + bs[8 * k + 2 * i];
+        float b = v[8 * k + 2 * i + 1] + bs[8 * k + 2 * i + 1];
+        if (ep.relu) {
+          a = fmaxf(a, 0.f);
+          b = fmaxf(b, 0.f);
+        }
+        if (ep.c_dtype == kF16) {
+          __half2 h = __floats2half2_rn(a, b);
+          pk[i] = *reinterpret_cast<uint32_t*>(&h);
+        } else {
+          __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+          pk[i] = *reinterpret_cast<uint32_t*>(&h);
+        }
+      }
+      row[k ^ ((lane >> 1) & 3)] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+    }
+  }
+  fence_proxy_async_smem();   // generic-proxy writes -> visible to the TMA engine
+  __syncwarp();
+  if (lane == 0) {
+    tma_store_2d(tmc, buf, nb, m0r);
+    bulk_commit();
+  }
+}
+
+template <int BN, int STAGES, int TOPK, bool I8 = false, int MINB = 1, int NACC = 2,
+          bool TS = false>
 __global__ void __launch_bounds__(kTcThreads, MINB)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmw,
-                   int K, uint32_t idesc, EpiParams ep, int tiles_n, int tiles) {
-  using Cfg = TcCfg<BN, STAGES, I8, TOPK, NACC>;
+                   const __grid_constant__ CUtensorMap tmc, int K, uint32_t idesc, EpiParams ep,
+                   int tiles_n, int tiles) {
+  using Cfg = TcCfg<BN, STAGES, I8, TOPK, NACC, TS>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -427,6 +488,9 @@ __global__ void __launch_bounds__(kTcThreads, MINB)
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+  // TS staging: 1024-byte aligned (the 128-byte swizzle period), after the barriers
+  uint8_t* ostage = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(tslot) + 16 + 1023) & ~static_cast<uintptr_t>(1023));
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -566,31 +630,50 @@ __global__ void __launch_bounds__(kTcThreads, MINB)
       } else {
         float best_v = -INFINITY;
         int best_i = -1;
+        if constexpr (TS) {
+          uint8_t* stg = ostage + (warp - 2) * kStageWarpBytes;
 #pragma unroll 1
-        for (int c = 0; c < BN / 64; ++c) {
-          float v[32];
-          tmem_ld32(taddr + c * 32, v);
-          const int nb = n0 + col0 + c * 32;
-          if constexpr (I8) {
-            if (row_ok && nb < ep.N) {
-              const int o = acc * BN + col0 + c * 32;
-              q_dequant_chunk(ep, m, v, qsc_s + o, qzp_s + o, qcs_s + o);
-            }
+          for (int c = 0; c < BN / 64; ++c) {
+            float v[32];
+            tmem_ld32(taddr + c * 32, v);
+            const int nb = n0 + col0 + c * 32;
+            if (nb < ep.N)
+              ts_store_chunk(ep, &tmc, stg + (c & 1) * 4096, lane, nb, m0 + quarter * 32, v,
+                             bs + col0 + c * 32);
           }
-          if (row_ok && nb < ep.N)
-            epilogue_chunk(ep, m, nb, v, bs + col0 + c * 32, best_v, best_i);
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(tempty + acc);
+        } else {
+#pragma unroll 1
+          for (int c = 0; c < BN / 64; ++c) {
+            float v[32];
+            tmem_ld32(taddr + c * 32, v);
+            const int nb = n0 + col0 + c * 32;
+            if constexpr (I8) {
+              if (row_ok && nb < ep.N) {
+                const int o = acc * BN + col0 + c * 32;
+                q_dequant_chunk(ep, m, v, qsc_s + o, qzp_s + o, qcs_s + o);
+              }
+            }
+            if (row_ok && nb < ep.N)
+              epilogue_chunk(ep, m, nb, v, bs + col0 + c * 32, best_v, best_i);
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(tempty + acc);
+          if (ep.epi == kEpiArgmax && row_ok && best_i >= 0)
+            atomicMax(ep.keys + m, argmax_key(best_v, (uint32_t)best_i));
         }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(tempty + acc);
-        if (ep.epi == kEpiArgmax && row_ok && best_i >= 0)
-          atomicMax(ep.keys + m, argmax_key(best_v, (uint32_t)best_i));
       }
       if (++acc == NACC) {
         acc = 0;
         aph ^= 1;
       }
     }
+  }
+  if constexpr (TS) {
+    if (warp >= 2 && lane == 0) bulk_wait_all();   // output stores complete before exit
   }
   tc_fence_before();
   __syncthreads();
@@ -683,14 +766,15 @@ int num_sms() {
 // MINB = 2: two co-resident CTAs per SM (half-depth stage ring, <= 96
 // registers) for the skinny decoder GEMMs, so a second tile (or another
 // decode lane's kernel) hides the TMA / MMA / epilogue latency of the first.
-template <int BN, int STAGES, int TOPK = 0, bool I8 = false, int MINB = 1, int NACC = 2>
+template <int BN, int STAGES, int TOPK = 0, bool I8 = false, int MINB = 1, int NACC = 2,
+          bool TS = false>
 cudaError_t launch_tc(const CUtensorMap& ta, const CUtensorMap& tw, const GemmArgs& g,
-                      const EpiParams& ep, cudaStream_t s) {
-  using Cfg = TcCfg<BN, STAGES, I8, TOPK, NACC>;
+                      const EpiParams& ep, cudaStream_t s, const CUtensorMap* tc = nullptr) {
+  using Cfg = TcCfg<BN, STAGES, I8, TOPK, NACC, TS>;
   static_assert(Cfg::kSmem <= 227 * 1024, "GEMM stage ring exceeds shared memory");
   static_assert(MINB == 1 || MINB * (Cfg::kSmem + 1024) <= 228 * 1024, "MINB CTAs do not fit");
   static_assert(MINB * NACC * BN <= 512, "co-resident CTAs exceed TMEM");
-  auto kern = gemm_tc_kernel<BN, STAGES, TOPK, I8, MINB, NACC>;
+  auto kern = gemm_tc_kernel<BN, STAGES, TOPK, I8, MINB, NACC, TS>;
   cudaError_t e = set_max_smem((const void*)kern);
   if (e != cudaSuccess) return e;
   const int tiles_n = (g.N + BN - 1) / BN;
@@ -698,7 +782,8 @@ cudaError_t launch_tc(const CUtensorMap& ta, const CUtensorMap& tw, const GemmAr
   const int grid = tiles < MINB * num_sms() ? tiles : MINB * num_sms();
   const uint32_t idesc = I8 ? umma_idesc_i8(kBM, BN) : umma_idesc_f16(kBM, BN, g.in_dtype == kBF16);
   return launch_k(kern, dim3(grid), dim3(kTcThreads),
-                  (size_t)Cfg::kSmem, s, ta, tw, I8 ? g.Kp : g.K, idesc, ep, tiles_n, tiles);
+                  (size_t)Cfg::kSmem, s, ta, tw, tc ? *tc : tw, I8 ? g.Kp : g.K, idesc, ep,
+                  tiles_n, tiles);
 }
 
 
@@ -722,6 +807,35 @@ bool pdl_enabled() {
     on = !(e && e[0] == '0');
   }
   return on != 0;
+}
+
+bool tma_store_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("FNMT_TMA_STORE");
+    on = !(e && e[0] == '0');
+  }
+  return on != 0;
+}
+
+// Output tensor map of a kEpiStore GEMM: [M, N] with leading dimension ldc,
+// box 32 columns x 32 rows, swizzled like ts_store_chunk writes the chunk.
+bool make_tmap_out(CUtensorMap* out, const void* base, int dtype, int64_t rows, int64_t cols,
+                   int64_t ld) {
+  auto fn = encode_fn();
+  const int es = dtype == kF32 ? 4 : 2;
+  if (!fn || (reinterpret_cast<uintptr_t>(base) & 15) || ((ld * es) & 15)) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * es)};
+  cuuint32_t box[2] = {32u, 32u};
+  cuuint32_t estr[2] = {1, 1};
+  const CUtensorMapDataType t = dtype == kF32    ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                : dtype == kBF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                                 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  return fn(out, t, 2, const_cast<void*>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE,
+            dtype == kF32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+            CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 bool make_tmap_16(CUtensorMap* out, const void* base, int dtype, int64_t rows, int64_t cols,
@@ -811,6 +925,15 @@ cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t s) {
                          : launch_tc<256, 4, 8>(*pa, *pw, g, ep, s);
   }
   const int bn = pick_bn(g.M, g.N, g.K);
+  CUtensorMap tc;
+  if (g.epi == kEpiStore && !g.resid && tma_store_enabled() &&
+      make_tmap_out(&tc, g.C, g.c_dtype, g.M, g.N, g.ldc)) {
+    switch (bn) {
+      case 256: return launch_tc<256, 3, 0, false, 1, 2, true>(*pa, *pw, g, ep, s, &tc);
+      case 128: return launch_tc<128, 4, 0, false, 1, 2, true>(*pa, *pw, g, ep, s, &tc);
+      default: return launch_tc<64, 5, 0, false, 1, 2, true>(*pa, *pw, g, ep, s, &tc);
+    }
+  }
   switch (bn) {
     case 256: return launch_tc<256, 4>(*pa, *pw, g, ep, s);
     case 128: return launch_tc<128, 6>(*pa, *pw, g, ep, s);

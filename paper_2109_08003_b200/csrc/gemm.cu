@@ -297,6 +297,20 @@ __device__ __forceinline__ void tile_coords(int tile, int tiles_n, int BN, int& 
 }
 
 
+__device__ __forceinline__ float4 lds_f4(const float* p) {
+  float4 r;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "r"(smem_u32(p)));
+  return r;
+}
+
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 // Beam epilogue for one row of a 256-column tile (kTopKTile): each of the two
 // warps of a TMEM lane quarter makes two passes over its 128-column half (max
 // + running top-K, then sum of exp(x - max)); the half-1 warp hands its
@@ -317,16 +331,38 @@ __device__ __forceinline__ void topk_epilogue(const EpiParams& ep, uint32_t tadd
     tv[j] = -INFINITY;
     ti[j] = -1;
   }
+  // pass 1: half-tile max and running top-K.  A chunk whose max does not beat
+  // the current K-th value cannot change the top-K, so the insertion network
+  // runs only for the (rare, after the first chunk) chunks that can.  The
+  // bias chunk comes from shared memory as 16-byte vectors.
+  constexpr float kLog2e = 1.4426950408889634f;
 #pragma unroll 1
   for (int c = 0; c < BN / 64; ++c) {
     float v[32];
     tmem_ld32(taddr + c * 32, v);
     const int nb = n0 + c * 32;
+    const int nv = min(32, ep.N - nb);   // valid columns of this chunk (may be <= 0)
+    float cm = -INFINITY;
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      const float x = v[i] + bs[c * 32 + i];
-      if (nb + i < ep.N) {
-        mx = fmaxf(mx, x);
+    for (int q = 0; q < 8; ++q) {
+      const float4 b = lds_f4(bs + c * 32 + 4 * q);
+      v[4 * q] += b.x;
+      v[4 * q + 1] += b.y;
+      v[4 * q + 2] += b.z;
+      v[4 * q + 3] += b.w;
+    }
+    if (nv < 32) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (i >= nv) v[i] = -INFINITY;
+    }
+#pragma unroll
+    for (int i = 0; i < 32; ++i) cm = fmaxf(cm, v[i]);
+    mx = fmaxf(mx, cm);
+    if (cm > tv[TOPK - 1]) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const float x = v[i];
         if (x > tv[TOPK - 1]) {
           tv[TOPK - 1] = x;
           ti[TOPK - 1] = nb + i;
@@ -345,17 +381,27 @@ __device__ __forceinline__ void topk_epilogue(const EpiParams& ep, uint32_t tadd
       }
     }
   }
+  // pass 2: sum of exp(x - max) over the valid columns, exp as 2^(x log2e -
+  // max log2e) on the MUFU (flush-to-zero: terms below 2^-126 vanish next to
+  // the max's 1)
   double sum = 0.0;
+  const float mxl = mx * kLog2e;
 #pragma unroll 1
   for (int c = 0; c < BN / 64; ++c) {
     float v[32];
     tmem_ld32(taddr + c * 32, v);
-    const int nb = n0 + c * 32;
+    const int nv = min(32, ep.N - (n0 + c * 32));
     float cs = 0.f;
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      const float x = v[i] + bs[c * 32 + i];
-      if (nb + i < ep.N) cs += exp2f((x - mx) * 1.4426950408889634f);
+    for (int q = 0; q < 8; ++q) {
+      const float4 b = lds_f4(bs + c * 32 + 4 * q);
+      const float x[4] = {v[4 * q] + b.x, v[4 * q + 1] + b.y, v[4 * q + 2] + b.z,
+                          v[4 * q + 3] + b.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float e = ex2_approx(fmaf(x[k], kLog2e, -mxl));
+        cs += (4 * q + k < nv) ? e : 0.f;
+      }
     }
     sum += (double)cs;
   }

@@ -407,6 +407,7 @@ def main():
     dist = dist_init(world, backend)
 
     from paper_2109_08003_b200 import store as S
+    from paper_2109_08003_b200.batching import estimate_device_bytes
     from paper_2109_08003_b200.engine import Engine, budgets_of
     from paper_2109_08003_b200.synthetic import newstest_corpus
 
@@ -417,6 +418,7 @@ def main():
     C = args.chunk_sentences
     n_chunks = max(1, CORPUS // C)
     eng = Engine(cfg, S.random_model(cfg, 0), dtype=args.dtype, device=local)
+    weight_bytes = eng.device_bytes()
     eng.reserve(SBATCH, WBATCH)
 
     chunk_meta = []
@@ -687,6 +689,12 @@ def main():
         "clocks": clocks,
         "peak_hbm_gb": round(max(peak_alloc, engine_bytes + peak_alloc) / 1e9, 3),
         "engine_device_gb": round(engine_bytes / 1e9, 3),
+        # weights (measured after load) + every decode lane's workspace from the
+        # allocation-level estimate (batching.estimate_device_bytes)
+        "engine_estimate_gb": round((weight_bytes + int(os.environ.get("FNMT_LANES", "4")) *
+                                     estimate_device_bytes(cfg, SBATCH, WBATCH,
+                                                           dtype_bytes=4 if args.dtype == "f32"
+                                                           else 2)) / 1e9, 3),
         "source_words_per_sec": round(src_all / t_max, 1),
         "sentences_per_sec": round(C * world * K / t_max, 1),
         "kernel_profile": kprof,

@@ -118,11 +118,21 @@ def estimate_peak_memory(plan: BatchPlan, cfg, max_out_len: int) -> int:
 
 def estimate_device_bytes(cfg, sbatch: int, wbatch: int, dtype_bytes: int = 2,
                           ratio: float = 1.5, offset: int = 5) -> int:
-    """Engine workspace at the given caps (csrc/engine.cu Engine::reserve)."""
-    d, fe, fd = cfg.d_model, cfg.ffn_dim_enc, max(cfg.ffn_dim_dec, 1)
+    """One decode lane's workspace at the given caps, allocation by allocation
+    as csrc/engine.cu Engine::reserve_for / Engine::reserve make it (greedy;
+    the folded single-head layout when the engine uses it).  The engine's total
+    is the weights plus this per lane (tests/test_gpu_memory.py checks it)."""
+    d, fe, fd = cfg.d_model, cfg.ffn_dim_enc, max(cfg.ffn_dim_dec, 8)
+    es = dtype_bytes
     tok = max(wbatch, cfg.max_positions)
+    rows = max(sbatch, 1)
     pool = max(math.ceil(ratio * wbatch) + (offset + 1) * sbatch, cfg.max_positions)
-    enc = tok * (4 * 2 * d + 4 * 3 + dtype_bytes * (d + 3 * d + d + fe))
-    dec = cfg.n_dec_layers * dtype_bytes * (tok * 2 * d + 2 * pool * d) + 4 * pool
-    rows = sbatch * (4 * 2 * d + dtype_bytes * (6 * d + fd) + 8 + 17)
-    return enc + dec + rows
+    folded = es != 4 and cfg.n_heads_dec == 1 and d % 256 == 0
+    act = lambda n: 0 if es == 4 else es * n   # noqa: E731  (fp32 engines alias the f32 buffer)
+    enc = 4 * tok * 2 + 4 * (rows + 1) + 4 * rows * 3 + 4 * tok * d * 2 + act(tok * d)
+    enc += es * tok * 3 * d + es * tok * d + es * tok * fe
+    row_w = 2 * d + 8 if folded else 2 * d
+    dec = cfg.n_dec_layers * (es * tok * row_w + es * pool * row_w)
+    step = 4 * rows * d * 2 + act(rows * d) + es * rows * (3 * d + d + d + fd)
+    step += 8 * rows + 4 * rows * 3 + rows + 4 * pool + 16
+    return enc + dec + step

@@ -297,6 +297,7 @@ class Engine {
   std::vector<DecL> dec;
   Workspace ws;
   cudaGraphExec_t graph_exec = nullptr;
+  std::vector<void*> graph_funcs;   // kernel functions of graph_exec's nodes, in node order
   cudaEvent_t ev_poll[2] = {nullptr, nullptr};
   cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr;
   int32_t* h_alive = nullptr;

@@ -256,6 +256,11 @@ struct StepKey {
   const float* pos_tab;
   void* knew;   // null: not used
   int w;
+  // multi-head q | k | v rows (kc set): columns [0, seg) -> knew[r, seg],
+  // [seg, 2 seg) -> kc[r cap + pos], [2 seg, 3 seg) -> vc[r cap + pos]
+  void* kc;
+  void* vc;
+  int seg, cap;
 };
 cudaError_t launch_step_key(const StepKey& k, const int32_t* tok, const int32_t* t_ptr, int rows,
                             int act_dtype, cudaStream_t s);

@@ -295,13 +295,25 @@ cudaError_t launch_add_norm(const float* x, const float* y, const float* gain, c
 // (fp32 sum, one rounding), 8 columns per lane and pass.
 template <typename TA>
 __device__ __forceinline__ void step_key_row(const StepKey& k, int r, int tok, int pos, int lane) {
+  if (k.kc && pos >= k.cap) return;   // no further step for this batch (cache slots end at cap)
   const float* tr = k.tok_tab + (size_t)tok * k.w;
   const float* pr = k.pos_tab + (size_t)pos * k.w;
-  TA* dst = reinterpret_cast<TA*>(k.knew) + (size_t)r * k.w;
   for (int c4 = lane; c4 < (k.w >> 2); c4 += 32) {
     const float4 a = reinterpret_cast<const float4*>(tr)[c4];
     const float4 b = reinterpret_cast<const float4*>(pr)[c4];
-    store4(dst + 4 * c4, make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w));
+    const float4 o = make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+    int c = 4 * c4;
+    TA* dst;
+    if (!k.kc) {
+      dst = reinterpret_cast<TA*>(k.knew) + (size_t)r * k.w + c;
+    } else {
+      const int sec = c / k.seg;
+      c -= sec * k.seg;
+      dst = sec == 0 ? reinterpret_cast<TA*>(k.knew) + (size_t)r * k.seg + c
+                     : reinterpret_cast<TA*>(sec == 1 ? k.kc : k.vc) +
+                           ((size_t)r * k.cap + pos) * k.seg + c;
+    }
+    store4(dst, o);
   }
 }
 
@@ -317,7 +329,7 @@ __global__ void __launch_bounds__(256) step_key_kernel(StepKey k, const int32_t*
 cudaError_t launch_step_key(const StepKey& k, const int32_t* tok, const int32_t* t_ptr, int rows,
                             int act_dtype, cudaStream_t s) {
   if (rows <= 0) return cudaSuccess;
-  if (k.w % 4) return cudaErrorInvalidValue;
+  if (k.w % 4 || (k.kc && k.seg % 4)) return cudaErrorInvalidValue;
   const dim3 grid((rows + 7) / 8);
   if (act_dtype == kF16) return launch_k(step_key_kernel<__half>, grid, dim3(256), 0, s, k, tok, t_ptr, rows);
   if (act_dtype == kBF16)

@@ -1,4 +1,3 @@
-timeout 900 python -m pytest tests/test_gpu_memory.py tests/test_gpu_fused_layer.py tests/test_gpu_corpus_parity.py -q -x -s -m gpu -k "memory or multi_head or s618" > gpurun_out/t_mh.log 2>&1; echo "tests rc=$?"
-grep -E "identical|parity:|passed|failed|Error|assert" gpurun_out/t_mh.log | cut -c1-200 | tail -6
-timeout 1500 compute-sanitizer --tool memcheck --print-limit 20 python -m pytest tests/test_gpu_parity.py tests/test_gpu_kernels.py tests/test_gpu_errors.py -q -x -m gpu -k "not random" > gpurun_out/memcheck_c.log 2>&1; echo "memcheck rc=$?"; tail -2 gpurun_out/memcheck_c.log
-FNMT_STEP_TABLES_MH=1 timeout 1500 compute-sanitizer --tool memcheck --print-limit 20 python -m pytest tests/test_gpu_parity.py -q -x -m gpu -k "protocol" > gpurun_out/memcheck_d.log 2>&1; echo "memcheck mh rc=$?"; tail -2 gpurun_out/memcheck_d.log
+timeout 600 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_parity.py -q -x -m gpu 2>&1 | tail -1
+python tools/perf_gemm.py > /tmp/a.txt; tail -4 /tmp/a.txt
+FNMT_TMA_STORE_SINGLE=0 python tools/perf_gemm.py > /tmp/b.txt; tail -4 /tmp/b.txt

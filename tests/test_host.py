@@ -286,3 +286,18 @@ def test_search_matches_oracle_on_small_models(golden):
         for k in (2, 4):
             want = split(g[f"{tag}__beam{k}_ids"], g[f"{tag}__beam{k}_lens"])
             assert beam_translate(m, enc, SearchConfig(2, 3, 0, beam_size=k)) == want
+
+
+def test_device_workspace_estimate_pinned():
+    """batching.estimate_device_bytes against the workspace the engine
+    allocated on a B200 (tests/test_gpu_memory.py, profiles/r02/
+    gpu_tests_summary.txt): the folded single-head, multi-head and fp32
+    layouts at the paper's caps and at small caps."""
+    from paper_2109_08003_b200 import store as S
+    from paper_2109_08003_b200.batching import estimate_device_bytes
+    measured = {(1, 2, 3072, 64000): 1265375252, (1, 2, 128, 2048): 41287316,
+                (8, 2, 3072, 64000): 1262520340, (8, 2, 128, 2048): 41193108,
+                (1, 4, 3072, 64000): 2111866900, (1, 4, 128, 2048): 68980372}
+    for (heads, es, sb, wb), want in measured.items():
+        cfg = S.ModelConfig(6, 1, 512, heads, heads, 2048, 2048, 32772, 1024)
+        assert estimate_device_bytes(cfg, sb, wb, dtype_bytes=es) == want, (heads, es, sb, wb)

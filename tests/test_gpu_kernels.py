@@ -38,7 +38,7 @@ def linear(A, W, bias, dt, out_dt=_capi.F32, relu=0, resid=None):
 
 SHAPES = [(1, 16, 16), (5, 48, 16), (77, 130, 64), (128, 128, 512), (300, 512, 512),
           (257, 1536, 512), (1000, 2048, 512), (999, 512, 2048), (64, 32772, 512),
-          (3, 96, 768), (130, 768, 3072)]
+          (3, 96, 768), (130, 768, 3072), (8200, 1536, 512), (8320, 512, 2048)]
 
 
 @pytest.mark.parametrize("dt", [_capi.F16, _capi.BF16])
@@ -84,9 +84,10 @@ def test_simt_fp32_gemm(M, N, K):
 
 
 @pytest.mark.parametrize("dt", [_capi.F16, _capi.F32])
-def test_fused_vocab_argmax_lowest_id_on_ties(dt):
+@pytest.mark.parametrize("M", [200, 1100])
+def test_fused_vocab_argmax_lowest_id_on_ties(dt, M):
     g = torch.Generator(device="cpu").manual_seed(11)
-    M, N, K = 200, 32772, 512
+    N, K = 32772, 512
     A = torch.randn(M, K, generator=g).to(DEV, TDT[dt])
     W = (torch.randn(N, K, generator=g) / 22.6).to(DEV, TDT[dt])
     W[7] = W[5]            # exact duplicate column -> tie between ids 5 and 7

@@ -585,6 +585,7 @@ def main():
 
     # ---- live per-kernel profile (one sub-chunk, events on the engine stream) --
     prof = None
+    prof_words = 0
     if rank == 0 and args.profile_sentences > 0:
         c = chunk_of(0)
         lo = chunk_meta[c][0]
@@ -599,6 +600,7 @@ def main():
                              wbatch=WBATCH, beam=BEAM)
         prof = eng.profile_read()
         eng.profile(False)
+        prof_words = int(d_out_len[0][:hi - lo].sum().item())
 
     if rank != 0:
         if world > 1:
@@ -640,8 +642,16 @@ def main():
                         "peak": hbm_peak, "unit": "GB/s", "frac": round(ach / hbm_peak, 4),
                         "traffic": traffic, "per_launch_ms": round(per_launch_ms, 4),
                         "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
-        # whole-step algorithmic rate (63.8 MFLOP / target word)
-        roofline["step_tflops"] = round(sum(p["flops"] for p in prof.values()) / (total_ms * 1e9), 2)
+        # whole-step algorithmic rate (63.8 MFLOP / target word) over the
+        # profile pass's summed kernel time, and the timed run's whole-path rate: the
+        # profile pass's algorithmic FLOPs per target word x the timed words / s
+        flops_total = sum(p["flops"] for p in prof.values())
+        roofline["step_tflops"] = round(flops_total / (total_ms * 1e9), 2)
+        if prof_words:
+            path = flops_total / prof_words * value / 1e12
+            roofline["path_mflop_per_word"] = round(flops_total / prof_words / 1e6, 2)
+            roofline["path_tflops"] = round(path, 1)
+            roofline["path_frac"] = round(path / tc_peak, 4)
 
     # ---- CPU baseline + parity on the timed workload -------------------------
     # The CPU arm translates the first sentences of the LAST timed e2e step's

@@ -196,8 +196,10 @@ Engine::Engine(const fnmt_arch& a, int device, int dtype) : arch(a), device(devi
   }
   CK(cudaSetDevice(device));
   CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
-  CK(cudaEventCreateWithFlags(&ev_poll[0], cudaEventDisableTiming));
-  CK(cudaEventCreateWithFlags(&ev_poll[1], cudaEventDisableTiming));
+  // blocking-sync poll events: a lane thread waiting on its alive count sleeps
+  // instead of spinning a host core (8 ranks x 4 lanes share one host at N = 8)
+  CK(cudaEventCreateWithFlags(&ev_poll[0], cudaEventDisableTiming | cudaEventBlockingSync));
+  CK(cudaEventCreateWithFlags(&ev_poll[1], cudaEventDisableTiming | cudaEventBlockingSync));
   CK(cudaEventCreate(&ev_t0));
   CK(cudaEventCreate(&ev_t1));
   CK(cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming));

@@ -493,7 +493,10 @@ Lin Engine::make_folded(const std::string& p, const std::string& blk, std::vecto
 // Step tables of a layer-0 folded self block (see DecL::tok_tab): true-fp32
 // GEMMs at load (gemm_simt_kernel, ascending-k FMA) of the scaled embedding
 // table E s (fp32, as embed computes it) and of the sinusoid table P with the
-// folded weights; the bias goes into the position table.
+// folded weights; the bias goes into the position table.  decode_step's layer-0
+// input is x = tgt_embed[prev] sqrt(d) + positions[t] (model.py:327-328) and its
+// self k / v projections (model.py:330-334, folded) are linear in x, so the
+// step's key row is tok_tab[prev] + pos_tab[t] (distributivity; one rounding).
 void Engine::make_step_tables(DecL& L, const std::vector<float>& wt,
                               const std::vector<float>& bias) {
   const int d = arch.d_model, N = (int)bias.size(), V = arch.vocab_size, np = arch.max_positions;

@@ -456,8 +456,9 @@ __device__ __forceinline__ void topk_epilogue(const EpiParams& ep, uint32_t tadd
   }
 }
 
-// Stage 32 rows x 32 columns of output (row = lane) into a swizzled chunk
-// buffer and TMA-store it at (column nb, row m0r).  fp16 / bf16: 64-byte rows,
+// TMA-store epilogue (Projection.apply's output, model.py:84-90): stage 32
+// rows x 32 columns of output (row = lane) into a swizzled chunk buffer and
+// TMA-store it at (column nb, row m0r).  fp16 / bf16: 64-byte rows,
 // SWIZZLE_64B (16-byte unit k of row r at k ^ ((r >> 1) & 3)); fp32: 128-byte
 // rows, SWIZZLE_128B (unit k at k ^ (r & 7)) -- conflict-free shared stores.
 __device__ __forceinline__ void ts_store_chunk(const EpiParams& ep, const CUtensorMap* tmc,

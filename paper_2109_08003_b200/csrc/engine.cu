@@ -263,6 +263,10 @@ Engine::~Engine() {
   if (stream) cudaStreamSynchronize(stream);
   for (void* p : allocations) cudaFree(p);
   if (h_alive) cudaFreeHost(h_alive);
+  if (h_live_tab) {
+    cudaEventDestroy(ev_live);
+    cudaFreeHost(h_live_tab);
+  }
   cudaEventDestroy(ev_poll[0]);
   cudaEventDestroy(ev_poll[1]);
   cudaEventDestroy(ev_t0);
@@ -562,6 +566,15 @@ bool step_tables_enabled() {
   return on != 0;
 }
 
+bool live_rows_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("FNMT_LIVE_ROWS");
+    on = !(e && e[0] == '0');
+  }
+  return on != 0;
+}
+
 bool greedy_embed_enabled() {
   static int on = -1;
   if (on < 0) {
@@ -814,6 +827,10 @@ void Engine::gemm(const void* A, const CUtensorMap* tmA, int lda, const Lin& L, 
   g.ld_resid = ldc;
   g.tmap_a = tmA;
   g.tmap_w = dt == kF32 ? nullptr : &L.tm;
+  if (step_m_tab && !q8) {
+    g.m_tab = step_m_tab;
+    g.t_ptr = step_t_ptr;
+  }
   attach_q(g, L);
   const int ev = prof_begin(s);
   CK(launch_gemm(g, s));
@@ -840,6 +857,10 @@ void Engine::gemm_argmax(const void* A, const CUtensorMap* tmA, int lda, int M,
   g.keys = keys;
   g.tmap_a = tmA;
   g.tmap_w = dt == kF32 ? nullptr : &out.tm;
+  if (step_m_tab && !q8) {
+    g.m_tab = step_m_tab;
+    g.t_ptr = step_t_ptr;
+  }
   attach_q(g, out);
   const int ev = prof_begin(s);
   CK(launch_gemm(g, s));
@@ -853,7 +874,7 @@ void Engine::norm(const float* x, const float* y, const Norm& n, float* o32, voi
                   cudaStream_t s) {
   const int ev = prof_begin(s);
   CK(launch_add_norm(x, y, n.g, n.b, arch.norm_l1, o32, dt == kF32 ? nullptr : oa,
-                     dt, rows, arch.d_model, s));
+                     dt, rows, arch.d_model, s, step_m_tab, step_t_ptr));
   prof_end(s, ev, FNMT_K_NORM, 0.0,
            (prof_m >= 0 ? prof_m : (double)rows) * arch.d_model *
                ((y ? 12.0 : 8.0) + (dt == kF32 ? 0 : dtype_size(dt))));
@@ -955,6 +976,8 @@ void Engine::run_step(const StepView& v, cudaStream_t s) {
   const double Rl = (profiling && v.prof_live) ? (double)(*v.prof_live)[v.host_t] : (double)R;
   const double Sl = (profiling && v.prof_src) ? (*v.prof_src)[v.host_t] : (double)R * v.max_k;
   prof_m = profiling ? Rl : -1.0;
+  step_m_tab = v.m_tab;
+  step_t_ptr = v.t_ptr;
   if (!v.embed_done) {
     const int ev = prof_begin(s);
     CK(launch_embed(v.prev, nullptr, v.t_ptr, tgt_emb32, pos32, emb_scale(), ws.dx32,
@@ -1218,6 +1241,8 @@ void Engine::run_step(const StepView& v, cudaStream_t s) {
     gemm_argmax(ws.dxa, tc ? &ws.tm_dxa : nullptr, d, R, v.keys, s);
   }
   prof_m = -1.0;
+  step_m_tab = nullptr;
+  step_t_ptr = nullptr;
 }
 
 float Engine::emb_scale() const { return (float)std::sqrt((double)arch.d_model); }
@@ -1533,6 +1558,28 @@ int Engine::decode_greedy(int R, int cap, int max_len, const fnmt_run& run,
   StepView v = step_view(R, cap, max_len, 1);
   v.keys = ws.keys;
   v.row_done = ws.finished;
+  // rows inside their budget at step t: the batch rows come length-descending
+  // (plan_batches), so budgets are non-increasing and the live rows at step t
+  // are the prefix [0, live[t]); the step's GEMMs and norm stop there
+  if (dt != kF32 && !q8 && live_rows_enabled() && cap > 0 &&
+      std::is_sorted(budgets.rbegin(), budgets.rend())) {
+    const size_t n_tab = (size_t)arch.max_positions + 2;
+    if (!d_live_tab) {
+      d_live_tab = (int32_t*)dalloc(sizeof(int32_t) * n_tab);
+      CK(cudaMallocHost(&h_live_tab, sizeof(int32_t) * n_tab));
+      CK(cudaEventCreateWithFlags(&ev_live, cudaEventDisableTiming | cudaEventBlockingSync));
+    } else {
+      CK(cudaEventSynchronize(ev_live));   // the previous batch's copy has read the buffer
+    }
+    for (int t = 0, r = R; t <= cap; ++t) {
+      while (r > 0 && budgets[r - 1] <= t) --r;
+      h_live_tab[t] = r;
+    }
+    CK(cudaMemcpyAsync(d_live_tab, h_live_tab, sizeof(int32_t) * (cap + 1),
+                       cudaMemcpyHostToDevice, stream));
+    CK(cudaEventRecord(ev_live, stream));
+    v.m_tab = d_live_tab;
+  }
   // profiler: rows still inside their budget at step t (random weights never
   // emit EOS; an EOS-finished row would still be counted, an upper bound)
   std::vector<int> live;

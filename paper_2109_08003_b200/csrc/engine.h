@@ -115,6 +115,7 @@ struct StepView {
   unsigned long long* keys = nullptr;  // argmax output (greedy)
   float* logits = nullptr;             // or full logits (protocol path / fp32 beam)
   const TopKPartials* topk = nullptr;  // beam: per-tile top-K partials
+  const int32_t* m_tab = nullptr;      // greedy: rows inside their budget at step t (GemmArgs::m_tab)
   bool embed_done = false;             // the decoder input was written by the previous
                                        // step's greedy update (greedy_embed_kernel)
 };
@@ -243,6 +244,12 @@ class Engine {
   size_t prof_used = 0;
   int gemm_cls = FNMT_K_GEMM_ENC;
   double prof_m = -1.0;   // >= 0: rows the profiler counts for GEMM / norm launches (live rows)
+  // decode-step GEMMs / norms stop at the rows inside their budget (run_step)
+  const int32_t* step_m_tab = nullptr;
+  const int32_t* step_t_ptr = nullptr;
+  int32_t* d_live_tab = nullptr;   // [max_positions + 2] live rows per step of the current batch
+  int32_t* h_live_tab = nullptr;   // pinned staging of d_live_tab
+  cudaEvent_t ev_live = nullptr;   // its copy has been issued / completed
 
   void* dalloc(size_t bytes);
   const std::vector<float>& need(const std::string& name, int64_t numel) const;

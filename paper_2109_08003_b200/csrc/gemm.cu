@@ -63,6 +63,7 @@ struct EpiParams {
   const int32_t* rowsum;
   const unsigned int* stats;
   int qk;
+  const int32_t* m_tab;   // GemmArgs::m_tab (with t_ptr)
 };
 
 // kEpiQKV destination of output element (m, n): q columns go to C, k / v
@@ -565,6 +566,11 @@ __global__ void __launch_bounds__(kTcThreads, MINB)
   // predecessor's tail; A (and everything else) is read only after this.
   pdl_trigger();
   pdl_wait();
+  // greedy decode: only the row blocks that still hold rows inside their budget
+  if (ep.m_tab) {
+    const int mv = min(ep.M, ep.m_tab[*ep.t_ptr]);
+    tiles = tiles_n * ((mv + kBM - 1) / kBM);
+  }
 
   if (warp == 0) {
     if (lane == 0) {
@@ -941,7 +947,8 @@ cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t s) {
   if (g.qw) return launch_qgemm(g, s);
   EpiParams ep{g.bias, g.M, g.N, g.epi, g.C, g.ldc, g.c_dtype, g.relu, g.resid, g.ld_resid,
                g.keys, g.topk, g.kc, g.vc, g.cap, g.seg, g.t_ptr,
-               nullptr, nullptr, nullptr, nullptr, nullptr, 0};
+               nullptr, nullptr, nullptr, nullptr, nullptr, 0, g.m_tab};
+  if (g.m_tab && (!g.t_ptr || g.epi == kEpiTopK)) return cudaErrorInvalidValue;
   if (g.epi == kEpiQKV && (!g.kc || !g.vc || !g.t_ptr || g.seg <= 0 || g.N != 3 * g.seg))
     return cudaErrorInvalidValue;
   if (g.epi == kEpiSlot && (!g.t_ptr || g.cap <= 0 || g.resid)) return cudaErrorInvalidValue;

@@ -108,6 +108,10 @@ struct GemmArgs {
   void* vc = nullptr;
   int cap = 0, seg = 0;
   const int32_t* t_ptr = nullptr;
+  // greedy decode steps: rows [m_tab[*t_ptr], M) are past their budgets this
+  // step (batch rows are in non-increasing budget order), so the GEMM stops
+  // there (null: all M rows)
+  const int32_t* m_tab = nullptr;
   // Pre-encoded TMA descriptors (tcgen05 path).  If null the launcher encodes
   // them on the fly (host cost ~ microseconds).
   const CUtensorMap* tmap_a = nullptr;
@@ -149,7 +153,8 @@ cudaError_t launch_embed(const int32_t* ids, const int32_t* pos_ids, const int32
 // out = norm(x + y) with gain/bias; variant 0 = l2, 1 = l1 (tensor.py:98-129)
 cudaError_t launch_add_norm(const float* x, const float* y, const float* gain,
                             const float* bias, int l1, float* out32, void* out_act,
-                            int act_dtype, int rows, int d, cudaStream_t s);
+                            int act_dtype, int rows, int d, cudaStream_t s,
+                            const int32_t* rows_tab = nullptr, const int32_t* t_ptr = nullptr);
 // same, the residual branch given as ny partial sums y + k * ystride (k < ny),
 // added in order ((y0 + y1) + y2) + ... (split-K GEMM outputs)
 

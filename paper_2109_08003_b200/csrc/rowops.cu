@@ -71,11 +71,12 @@ template <typename TA, int NV>
 __global__ void add_norm_kernel(const float* __restrict__ x, const float* __restrict__ y,
                                 const float* __restrict__ gain, const float* __restrict__ bias,
                                 int l1, float* __restrict__ out32, TA* __restrict__ out_act,
-                                int rows, int d) {
+                                int rows, int d, const int32_t* rows_tab, const int32_t* t_ptr) {
   pdl_trigger();
   pdl_wait();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
+  if (rows_tab) rows = min(rows, rows_tab[*t_ptr]);   // rows past their budgets: skipped
   if (warp >= rows) return;
   const int d4 = d >> 2;
   const float* xr = x + (size_t)warp * d;
@@ -140,12 +141,13 @@ __global__ void add_norm_kernel(const float* __restrict__ x, const float* __rest
 
 template <typename TA>
 cudaError_t add_norm_dispatch(const float* x, const float* y, const float* g, const float* b,
-                              int l1, float* o32, TA* oa, int rows, int d, cudaStream_t s) {
+                              int l1, float* o32, TA* oa, int rows, int d, cudaStream_t s,
+                              const int32_t* rows_tab = nullptr, const int32_t* t_ptr = nullptr) {
   const int threads = 256;
   const int blocks = (int)(((int64_t)rows * 32 + threads - 1) / threads);
   const int nv = (d / 4 + 31) / 32;
-  void (*k)(const float*, const float*, const float*, const float*, int, float*, TA*, int, int) =
-      nullptr;
+  void (*k)(const float*, const float*, const float*, const float*, int, float*, TA*, int, int,
+            const int32_t*, const int32_t*) = nullptr;
   if (nv <= 1)
     k = add_norm_kernel<TA, 1>;
   else if (nv <= 2)
@@ -160,7 +162,8 @@ cudaError_t add_norm_dispatch(const float* x, const float* y, const float* g, co
     k = add_norm_kernel<TA, 16>;
   else
     return cudaErrorInvalidValue;
-  return launch_k(k, dim3(blocks), dim3(threads), 0, s, x, y, g, b, l1, o32, oa, rows, d);
+  return launch_k(k, dim3(blocks), dim3(threads), 0, s, x, y, g, b, l1, o32, oa, rows, d,
+                  rows_tab, t_ptr);
 }
 
 // Single CTA: every row reads the same step counter, then thread 0 bumps it.
@@ -280,15 +283,17 @@ cudaError_t launch_embed(const int32_t* ids, const int32_t* pos_ids, const int32
 
 cudaError_t launch_add_norm(const float* x, const float* y, const float* gain, const float* bias,
                             int l1, float* out32, void* out_act, int act_dtype, int rows, int d,
-                            cudaStream_t s) {
+                            cudaStream_t s, const int32_t* rows_tab, const int32_t* t_ptr) {
   if (rows <= 0) return cudaSuccess;
-  if (d % 4) return cudaErrorInvalidValue;
+  if (d % 4 || (rows_tab && !t_ptr)) return cudaErrorInvalidValue;
   if (act_dtype == kF16 || !out_act)
-    return add_norm_dispatch<__half>(x, y, gain, bias, l1, out32, (__half*)out_act, rows, d, s);
+    return add_norm_dispatch<__half>(x, y, gain, bias, l1, out32, (__half*)out_act, rows, d, s,
+                                     rows_tab, t_ptr);
   if (act_dtype == kBF16)
     return add_norm_dispatch<__nv_bfloat16>(x, y, gain, bias, l1, out32,
-                                            (__nv_bfloat16*)out_act, rows, d, s);
-  return add_norm_dispatch<float>(x, y, gain, bias, l1, out32, (float*)out_act, rows, d, s);
+                                            (__nv_bfloat16*)out_act, rows, d, s, rows_tab, t_ptr);
+  return add_norm_dispatch<float>(x, y, gain, bias, l1, out32, (float*)out_act, rows, d, s,
+                                  rows_tab, t_ptr);
 }
 
 // One warp writes row r's layer-0 self key: act(tok_tab[tok] + pos_tab[pos])

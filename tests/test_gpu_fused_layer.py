@@ -108,3 +108,14 @@ def test_multi_head_step_tables_match_qkv_gemm(tmp_path):
     print("8-head step tables vs QKV GEMM identical:", same, "/", N, "launches", la, "vs", lb)
     assert same >= 0.99 * N
     assert la < lb
+
+
+def test_live_row_bound_is_output_neutral(tmp_path):
+    """Decode-step GEMMs and the norm stop at the rows still inside their
+    budget (batch rows are length-descending, so those rows are a prefix;
+    engine.cu decode_greedy / GemmArgs::m_tab): the rows past their budgets are
+    finished and discarded (search.py:72-74), so the outputs are identical."""
+    a, la = run(tmp_path, "f16", True)
+    b, lb = run(tmp_path, "f16", True, FNMT_LIVE_ROWS="0")
+    assert a == b
+    assert la == lb

@@ -1486,7 +1486,9 @@ int64_t Engine::run_batch(const PlanCtx& P, size_t bi) {
       }
       steps_total += decode_greedy(R, cap, b.max_len, run, src, bud);
     } else {
-      steps_total += decode_beam(R, cap, b.max_len, run);
+      std::vector<int32_t> bud(R);
+      for (int r = 0; r < R; ++r) bud[r] = P.budget_all[P.batch_row0[bi] + r];
+      steps_total += decode_beam(R, cap, b.max_len, run, bud);
       res_ids = beam.out_ids;
       res_len = beam.out_len;
     }
@@ -1549,6 +1551,33 @@ StepView Engine::step_view(int rows, int cap, int max_len, int rows_per_seq) {
   return v;
 }
 
+// Rows inside their budget at each step t of a batch, uploaded for the
+// decode-step GEMMs / norm (GemmArgs::m_tab).  The batch's sentences come
+// length-descending (plan_batches), so budgets are non-increasing and the live
+// rows at step t are the prefix [0, mult * #{budget > t}) (mult = beam rows
+// per sentence).  Null when the order does not hold or the bound is off.
+const int32_t* Engine::live_table(const std::vector<int32_t>& budgets, int cap, int mult) {
+  if (dt == kF32 || q8 || !live_rows_enabled() || cap <= 0 || budgets.empty() ||
+      !std::is_sorted(budgets.rbegin(), budgets.rend()))
+    return nullptr;
+  const size_t n_tab = (size_t)arch.max_positions + 2;
+  if (!d_live_tab) {
+    d_live_tab = (int32_t*)dalloc(sizeof(int32_t) * n_tab);
+    CK(cudaMallocHost(&h_live_tab, sizeof(int32_t) * n_tab));
+    CK(cudaEventCreateWithFlags(&ev_live, cudaEventDisableTiming | cudaEventBlockingSync));
+  } else {
+    CK(cudaEventSynchronize(ev_live));   // the previous batch's copy has read the buffer
+  }
+  for (int t = 0, r = (int)budgets.size(); t <= cap; ++t) {
+    while (r > 0 && budgets[r - 1] <= t) --r;
+    h_live_tab[t] = r * mult;
+  }
+  CK(cudaMemcpyAsync(d_live_tab, h_live_tab, sizeof(int32_t) * (cap + 1), cudaMemcpyHostToDevice,
+                     stream));
+  CK(cudaEventRecord(ev_live, stream));
+  return d_live_tab;
+}
+
 int Engine::decode_greedy(int R, int cap, int max_len, const fnmt_run& run,
                           const std::vector<int32_t>& src_len, const std::vector<int32_t>& budgets) {
   init_decode_kernel<<<(R + 255) / 256, 256, 0, stream>>>(ws.prev, ws.finished, ws.out_len,
@@ -1558,28 +1587,8 @@ int Engine::decode_greedy(int R, int cap, int max_len, const fnmt_run& run,
   StepView v = step_view(R, cap, max_len, 1);
   v.keys = ws.keys;
   v.row_done = ws.finished;
-  // rows inside their budget at step t: the batch rows come length-descending
-  // (plan_batches), so budgets are non-increasing and the live rows at step t
-  // are the prefix [0, live[t]); the step's GEMMs and norm stop there
-  if (dt != kF32 && !q8 && live_rows_enabled() && cap > 0 &&
-      std::is_sorted(budgets.rbegin(), budgets.rend())) {
-    const size_t n_tab = (size_t)arch.max_positions + 2;
-    if (!d_live_tab) {
-      d_live_tab = (int32_t*)dalloc(sizeof(int32_t) * n_tab);
-      CK(cudaMallocHost(&h_live_tab, sizeof(int32_t) * n_tab));
-      CK(cudaEventCreateWithFlags(&ev_live, cudaEventDisableTiming | cudaEventBlockingSync));
-    } else {
-      CK(cudaEventSynchronize(ev_live));   // the previous batch's copy has read the buffer
-    }
-    for (int t = 0, r = R; t <= cap; ++t) {
-      while (r > 0 && budgets[r - 1] <= t) --r;
-      h_live_tab[t] = r;
-    }
-    CK(cudaMemcpyAsync(d_live_tab, h_live_tab, sizeof(int32_t) * (cap + 1),
-                       cudaMemcpyHostToDevice, stream));
-    CK(cudaEventRecord(ev_live, stream));
-    v.m_tab = d_live_tab;
-  }
+  // rows inside their budget at step t (decode-step GEMMs / norm stop there)
+  v.m_tab = live_table(budgets, cap, 1);
   // profiler: rows still inside their budget at step t (random weights never
   // emit EOS; an EOS-finished row would still be counted, an upper bound)
   std::vector<int> live;
@@ -1712,7 +1721,8 @@ void Engine::reserve_beam(int sent_cap, int k, int64_t pool_cap) {
   beam.bytes = device_bytes - before;
 }
 
-int Engine::decode_beam(int R, int cap, int max_len, const fnmt_run& run) {
+int Engine::decode_beam(int R, int cap, int max_len, const fnmt_run& run,
+                        const std::vector<int32_t>& budgets) {
   const int k = run.beam_size;
   const int rows = R * k;
   BeamState bs;
@@ -1753,6 +1763,7 @@ int Engine::decode_beam(int R, int cap, int max_len, const fnmt_run& run) {
   v.anc = beam.anc;
   v.anc_stride = (int64_t)rows * cap;
   v.topk = &beam.part;
+  v.m_tab = live_table(budgets, cap, k);   // the top-K vocab GEMM keeps all rows
   v.logits = dt == kF32 ? beam.logits : nullptr;
   auto body = [&](int t) {
     v.host_t = t;

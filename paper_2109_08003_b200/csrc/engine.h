@@ -286,7 +286,9 @@ class Engine {
   StepView step_view(int rows, int cap, int max_len, int rows_per_seq);
   int decode_greedy(int R, int cap, int max_len, const fnmt_run& run,
                     const std::vector<int32_t>& src_len, const std::vector<int32_t>& budgets);
-  int decode_beam(int R, int cap, int max_len, const fnmt_run& run);
+  int decode_beam(int R, int cap, int max_len, const fnmt_run& run,
+                  const std::vector<int32_t>& budgets);
+  const int32_t* live_table(const std::vector<int32_t>& budgets, int cap, int mult);
   void reserve_beam(int sent_cap, int k, int64_t pool_cap);
   BeamWs beam;
   void lens_from_cu(int R);

@@ -22,7 +22,7 @@ does not.  Work is spread over the host cores with one process per core
 (OMP_NUM_THREADS=1; the reference's einsum is batch-invariant, so the
 grouping does not change any value).
 
-Usage: python oracle/make_golden_corpus.py [greedy|beam|all]
+Usage: python oracle/make_golden_corpus.py [greedy|beam|all|greedy_wide]
 """
 
 from __future__ import annotations
@@ -47,6 +47,9 @@ CHUNK = 65536
 # (tag, STUDENTS key, beam, sample indices inside chunk 0)
 GREEDY = [("s611", "student_6_1_1", np.arange(1024) * 64),
           ("s618", "student_6_1_8", np.arange(512) * 128 + 17)]
+# a wider Student-6-1-8 sample (2048 sentences, disjoint from s618) for the
+# multi-head step-table decision (tests/test_gpu_corpus_parity.py)
+GREEDY_WIDE = [("s618_wide", "student_6_1_8", np.arange(2048) * 32 + 3)]
 BEAM = [("s668_beam4", "student_6_6_8", np.arange(32) * 256 + 5),
         ("deep_beam4", "deep_12_768", np.arange(24) * 341 + 9)]
 BEAM_K = 4
@@ -132,9 +135,9 @@ def _setup(key, with_oracle=False):
         _S["params"] = O.params_from_weights(a, w)
 
 
-def run_greedy(procs):
+def run_greedy(procs, sets=GREEDY):
     ids, off = corpus()
-    for tag, key, idx in GREEDY:
+    for tag, key, idx in sets:
         t0 = time.time()
         _setup(key)
         rows = [ids[off[i]:off[i + 1]].astype(np.int64) for i in idx]
@@ -179,5 +182,7 @@ if __name__ == "__main__":
     procs = os.cpu_count() or 1
     if what in ("greedy", "all"):
         run_greedy(procs)
+    if what == "greedy_wide":
+        run_greedy(procs, GREEDY_WIDE)
     if what in ("beam", "all"):
         run_beam(procs)

@@ -112,3 +112,41 @@ def test_production_vocab_logits_fp16(corpus, tag):
         assert err <= 1e-2, (t, err)
         prev = want.argmax(axis=1).astype(np.int64)
     print(tag, "worst fp16 logits rel err", worst)
+
+
+WIDE_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+from paper_2109_08003_b200 import store as S
+from paper_2109_08003_b200.engine import Engine
+from paper_2109_08003_b200.synthetic import newstest_corpus
+ids, off, _ = newstest_corpus(1 << 20, 32772)
+cfg = S.ModelConfig(6, 1, 512, 8, 8, 2048, 2048, 32772, 1024)
+eng = Engine(cfg, S.random_model(cfg, 0), dtype="f16")
+out, olen, oof, _ = eng.translate(ids, off[:65536 + 1], sbatch=3072, wbatch=64000)
+np.savez(sys.argv[2], out=out, olen=olen, oof=oof)
+"""
+
+
+@pytest.mark.parametrize("mh_tables", ["0", "1"])
+def test_greedy_corpus_wide_s618(golden, tmp_path, mh_tables):
+    """Config 3 on a wider, disjoint sample (2048 sentences of chunk 0,
+    corpus_s618_wide.npz), with and without the multi-head layer-0 step tables
+    (FNMT_STEP_TABLES_MH, a process-wide switch: each variant runs in its own
+    process): both at the north-star bar."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    fx = golden("corpus_s618_wide")
+    f = tmp_path / f"wide_{mh_tables}.npz"
+    env = dict(os.environ, FNMT_STEP_TABLES_MH=mh_tables)
+    root = Path(__file__).resolve().parent.parent
+    r = subprocess.run([sys.executable, "-c", WIDE_SCRIPT, str(root), str(f)], env=env,
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = np.load(f)
+    rep = P.greedy_report(rows_at(d["out"], d["olen"], d["oof"], fx["idx"]), fx)
+    print("s618_wide mh_tables", mh_tables, "fp16 greedy parity:",
+          {k: rep[k] for k in ("sentences", "identical", "identical_frac", "all_near_ties")})
+    assert rep["pass"], rep

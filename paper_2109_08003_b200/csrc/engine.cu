@@ -877,7 +877,7 @@ void Engine::norm(const float* x, const float* y, const Norm& n, float* o32, voi
                      dt, rows, arch.d_model, s, step_m_tab, step_t_ptr));
   prof_end(s, ev, FNMT_K_NORM, 0.0,
            (prof_m >= 0 ? prof_m : (double)rows) * arch.d_model *
-               ((y ? 12.0 : 8.0) + (dt == kF32 ? 0 : dtype_size(dt))));
+               ((y ? 8.0 : 4.0) + (o32 ? 4.0 : 0.0) + (dt == kF32 ? 0 : dtype_size(dt))));
   ++launches;
 }
 
@@ -886,9 +886,10 @@ void Engine::norm(const float* x, const float* y, const Norm& n, float* o32, voi
 // GEMM + LayerNorm epilogue exchanging row statistics over DSMEM 4.23M vs 6.81M: the
 // row-local epilogue serialises behind the 1-deep TMEM double buffer.)
 void Engine::gemm_norm(const void* A, const CUtensorMap* tmA, int lda, const Lin& L, int M,
-                       float* x32, void* xa, float* y32, const Norm& n, cudaStream_t s) {
+                       float* x32, void* xa, float* y32, const Norm& n, cudaStream_t s,
+                       bool keep32) {
   gemm(A, tmA, lda, L, M, y32, L.N, kF32, 0, s);
-  norm(x32, y32, n, x32, xa, M, s);
+  norm(x32, y32, n, keep32 ? x32 : nullptr, xa, M, s);
 }
 
 // Encoder over rows already embedded in ws.x32 / ws.xa (model.py:279-286).
@@ -1205,8 +1206,10 @@ void Engine::run_step(const StepView& v, cudaStream_t s) {
     }
     if (L.ffn) {
       gemm(ws.dxa, tc ? &ws.tm_dxa : nullptr, d, L.f1, R, ws.dh, arch.ffn_dim_dec, dt, 1, s);
+      // the last layer's fp32 residual stream has no reader (the vocabulary
+      // projection takes the activation copy; the next step re-embeds)
       gemm_norm(ws.dh, tc ? &ws.tm_dh : nullptr, arch.ffn_dim_dec, L.f2, R, ws.dx32, ws.dxa,
-                ws.dy32, L.n3, s);
+                ws.dy32, L.n3, s, dt == kF32 || l + 1 < arch.n_dec_layers);
     }
   }
   if (v.topk && tc) {

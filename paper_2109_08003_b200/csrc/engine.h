@@ -275,7 +275,7 @@ class Engine {
             cudaStream_t s);
   // x32 = norm(x32 + A.W + b) (and its storage-dtype copy xa): GEMM + add_norm.
   void gemm_norm(const void* A, const CUtensorMap* tmA, int lda, const Lin& L, int M, float* x32,
-                 void* xa, float* y32, const Norm& n, cudaStream_t s);
+                 void* xa, float* y32, const Norm& n, cudaStream_t s, bool keep32 = true);
   void encoder_layers(int n_tok, int n_seq, int max_q, int max_k, const int32_t* qstart,
                       const int32_t* qlen, const int32_t* kstart, const int32_t* klen, int k_pad,
                       cudaStream_t s);

@@ -66,7 +66,10 @@ __global__ void embed_kernel(const int32_t* __restrict__ ids, const int32_t* __r
   }
 }
 
-// One warp per row; each lane holds up to NV float4 chunks of the row.
+// One warp per row; each lane holds up to NV float4 chunks of the row.  The
+// row, gain and bias loads are all issued before the live-row bound is read
+// (rows past the bound are in the buffer, their values are just not used),
+// so a row costs one memory round trip before the two reductions.
 template <typename TA, int NV>
 __global__ void add_norm_kernel(const float* __restrict__ x, const float* __restrict__ y,
                                 const float* __restrict__ gain, const float* __restrict__ bias,
@@ -76,26 +79,36 @@ __global__ void add_norm_kernel(const float* __restrict__ x, const float* __rest
   pdl_wait();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (rows_tab) rows = min(rows, rows_tab[*t_ptr]);   // rows past their budgets: skipped
   if (warp >= rows) return;
   const int d4 = d >> 2;
   const float* xr = x + (size_t)warp * d;
   const float* yr = y ? y + (size_t)warp * d : nullptr;
-  float4 v[NV];
+  float4 v[NV], gv[NV], bv[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int c = lane + 32 * i;
+    if (c < d4) {
+      v[i] = reinterpret_cast<const float4*>(xr)[c];
+      if (yr) gv[i] = reinterpret_cast<const float4*>(yr)[c];
+    }
+  }
+  if (rows_tab && warp >= rows_tab[*t_ptr]) return;   // rows past their budgets: skipped
   double s = 0.0;
 #pragma unroll
   for (int i = 0; i < NV; ++i) {
     const int c = lane + 32 * i;
     if (c < d4) {
-      float4 a = reinterpret_cast<const float4*>(xr)[c];
+      float4 a = v[i];
       if (yr) {
-        const float4 b = reinterpret_cast<const float4*>(yr)[c];
+        const float4 b = gv[i];
         a.x = a.x + b.x;
         a.y = a.y + b.y;
         a.z = a.z + b.z;
         a.w = a.w + b.w;
       }
       v[i] = a;
+      gv[i] = reinterpret_cast<const float4*>(gain)[c];
+      bv[i] = reinterpret_cast<const float4*>(bias)[c];
       s += (double)a.x + (double)a.y + (double)a.z + (double)a.w;
     }
   }
@@ -126,8 +139,8 @@ __global__ void add_norm_kernel(const float* __restrict__ x, const float* __rest
   for (int i = 0; i < NV; ++i) {
     const int c = lane + 32 * i;
     if (c < d4) {
-      const float4 g = reinterpret_cast<const float4*>(gain)[c];
-      const float4 b = reinterpret_cast<const float4*>(bias)[c];
+      const float4 g = gv[i];
+      const float4 b = bv[i];
       float4 o;
       o.x = g.x * v[i].x / den + b.x;
       o.y = g.y * v[i].y / den + b.y;
@@ -296,38 +309,67 @@ cudaError_t launch_add_norm(const float* x, const float* y, const float* gain, c
                                   rows_tab, t_ptr);
 }
 
-// One warp writes row r's layer-0 self key: act(tok_tab[tok] + pos_tab[pos])
-// (fp32 sum, one rounding), 8 columns per lane and pass.
-template <typename TA>
-__device__ __forceinline__ void step_key_row(const StepKey& k, int r, int tok, int pos, int lane) {
-  if (k.kc && pos >= k.cap) return;   // no further step for this batch (cache slots end at cap)
-  const float* tr = k.tok_tab + (size_t)tok * k.w;
-  const float* pr = k.pos_tab + (size_t)pos * k.w;
-  for (int c4 = lane; c4 < (k.w >> 2); c4 += 32) {
-    const float4 a = reinterpret_cast<const float4*>(tr)[c4];
-    const float4 b = reinterpret_cast<const float4*>(pr)[c4];
-    const float4 o = make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
-    int c = 4 * c4;
-    TA* dst;
-    if (!k.kc) {
-      dst = reinterpret_cast<TA*>(k.knew) + (size_t)r * k.w + c;
-    } else {
-      const int sec = c / k.seg;
-      c -= sec * k.seg;
-      dst = sec == 0 ? reinterpret_cast<TA*>(k.knew) + (size_t)r * k.seg + c
-                     : reinterpret_cast<TA*>(sec == 1 ? k.kc : k.vc) +
-                           ((size_t)r * k.cap + pos) * k.seg + c;
+// Row map of the step kernels: out[c] = f(a[c], b[c]) over n4 float4 columns
+// of two read-only table rows, one warp per row.  Each lane issues all U of
+// its loads (both rows) before its first store, so a row costs one L2 round
+// trip per 32 U columns instead of one per 32 (the stores may alias nothing
+// the loads read, but the compiler cannot know that through plain pointers).
+template <int U, typename F>
+__device__ __forceinline__ void row_map4(const float* a, const float* b, int n4, int lane,
+                                         F&& put) {
+  const float4* a4 = reinterpret_cast<const float4*>(a);
+  const float4* b4 = reinterpret_cast<const float4*>(b);
+  for (int base = 0; base < n4; base += 32 * U) {
+    float4 va[U], vb[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int c = base + lane + 32 * u;
+      if (c < n4) {
+        va[u] = __ldg(a4 + c);
+        vb[u] = __ldg(b4 + c);
+      }
     }
-    store4(dst, o);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int c = base + lane + 32 * u;
+      if (c < n4) put(4 * c, va[u], vb[u]);
+    }
   }
 }
 
+constexpr int kKeyU = 9;   // w = 2 d + 8 = 1032 (d = 512): 258 float4 -> one pass
+constexpr int kEmbU = 4;   // d = 512: 128 float4 -> one pass
+
+// One warp writes row r's layer-0 self key: act(tok_tab[tok] + pos_tab[pos])
+// (fp32 sum, one rounding).
 template <typename TA>
-__global__ void __launch_bounds__(256) step_key_kernel(StepKey k, const int32_t* tok,
-                                                       const int32_t* t_ptr, int rows) {
+__device__ __forceinline__ void step_key_row(const StepKey& k, int r, int tok, int pos, int lane) {
+  if (k.kc && pos >= k.cap) return;   // no further step for this batch (cache slots end at cap)
+  row_map4<kKeyU>(k.tok_tab + (size_t)tok * k.w, k.pos_tab + (size_t)pos * k.w, k.w >> 2, lane,
+                  [&](int c, float4 a, float4 b) {
+                    const float4 o = make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+                    TA* dst;
+                    if (!k.kc) {
+                      dst = reinterpret_cast<TA*>(k.knew) + (size_t)r * k.w + c;
+                    } else {
+                      const int sec = c / k.seg;
+                      c -= sec * k.seg;
+                      dst = sec == 0 ? reinterpret_cast<TA*>(k.knew) + (size_t)r * k.seg + c
+                                     : reinterpret_cast<TA*>(sec == 1 ? k.kc : k.vc) +
+                                           ((size_t)r * k.cap + pos) * k.seg + c;
+                    }
+                    store4(dst, o);
+                  });
+}
+
+constexpr int kStepRows = 4;   // rows (warps) per CTA of the step kernels
+
+template <typename TA>
+__global__ void __launch_bounds__(32 * kStepRows) step_key_kernel(StepKey k, const int32_t* tok,
+                                                                  const int32_t* t_ptr, int rows) {
   pdl_trigger();
   pdl_wait();
-  const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int r = blockIdx.x * kStepRows + (threadIdx.x >> 5);
   if (r < rows) step_key_row<TA>(k, r, tok[r], *t_ptr, threadIdx.x & 31);
 }
 
@@ -335,10 +377,10 @@ cudaError_t launch_step_key(const StepKey& k, const int32_t* tok, const int32_t*
                             int act_dtype, cudaStream_t s) {
   if (rows <= 0) return cudaSuccess;
   if (k.w % 4 || (k.kc && k.seg % 4)) return cudaErrorInvalidValue;
-  const dim3 grid((rows + 7) / 8);
-  if (act_dtype == kF16) return launch_k(step_key_kernel<__half>, grid, dim3(256), 0, s, k, tok, t_ptr, rows);
+  const dim3 grid((rows + kStepRows - 1) / kStepRows), block(32 * kStepRows);
+  if (act_dtype == kF16) return launch_k(step_key_kernel<__half>, grid, block, 0, s, k, tok, t_ptr, rows);
   if (act_dtype == kBF16)
-    return launch_k(step_key_kernel<__nv_bfloat16>, grid, dim3(256), 0, s, k, tok, t_ptr, rows);
+    return launch_k(step_key_kernel<__nv_bfloat16>, grid, block, 0, s, k, tok, t_ptr, rows);
   return cudaErrorInvalidValue;
 }
 
@@ -348,22 +390,30 @@ cudaError_t launch_step_key(const StepKey& k, const int32_t* tok, const int32_t*
 // writes E[prev] * sqrt(d) + P[t + 1] (prev = the emitted token, or PAD for a
 // finished row) as the next step's residual stream and activation copy.  The
 // step counter is bumped by the last CTA to finish (every CTA has read t by
-// then), which also publishes the alive count.
+// then), which also publishes the alive count.  Lane 0's row state is read
+// together with the step counter (it does not depend on t).
 template <typename TA>
-__global__ void __launch_bounds__(256) greedy_embed_kernel(GreedyState g, GreedyEmbed e) {
+__global__ void __launch_bounds__(32 * kStepRows) greedy_embed_kernel(GreedyState g, GreedyEmbed e) {
   pdl_trigger();
   pdl_wait();
   __shared__ int alive_s;
-  const int t = *g.t;
   const int lane = threadIdx.x & 31;
-  const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int r = blockIdx.x * kStepRows + (threadIdx.x >> 5);
+  const bool lead = r < g.rows && lane == 0;
+  unsigned long long key = 0ull;
+  int fin = 1, budget = 0;
+  if (lead) {
+    key = g.keys[r];
+    fin = g.finished[r];
+    budget = g.budget[r];
+  }
+  const int t = *g.t;
   if (threadIdx.x == 0) alive_s = 0;
   __syncthreads();
   int tok = g.pad, alive = 0;
-  if (r < g.rows && lane == 0) {
-    const unsigned long long key = g.keys[r];
+  if (lead) {
     g.keys[r] = 0ull;
-    if (!g.finished[r]) {
+    if (!fin) {
       const int w = (int)argmax_key_index(key);
       if (w == g.eos) {
         g.finished[r] = 1;
@@ -371,7 +421,7 @@ __global__ void __launch_bounds__(256) greedy_embed_kernel(GreedyState g, Greedy
         if (t < g.out_cap) g.out_ids[(size_t)r * g.out_cap + t] = w;
         g.out_len[r] = t + 1;
         tok = w;
-        if (t + 1 >= g.budget[r])
+        if (t + 1 >= budget)
           g.finished[r] = 1;
         else
           alive = 1;
@@ -381,20 +431,19 @@ __global__ void __launch_bounds__(256) greedy_embed_kernel(GreedyState g, Greedy
   }
   tok = __shfl_sync(0xffffffffu, tok, 0);
   if (r < g.rows && t + 1 < e.n_pos) {
-    const int d4 = e.d >> 2;
-    const float* er = e.table + (size_t)tok * e.d;
-    const float* pr = e.pos + (size_t)(t + 1) * e.d;
-    for (int c4 = lane; c4 < d4; c4 += 32) {
-      const float4 a = reinterpret_cast<const float4*>(er)[c4];
-      const float4 q = reinterpret_cast<const float4*>(pr)[c4];
-      float4 o;
-      o.x = __fadd_rn(__fmul_rn(a.x, e.scale), q.x);
-      o.y = __fadd_rn(__fmul_rn(a.y, e.scale), q.y);
-      o.z = __fadd_rn(__fmul_rn(a.z, e.scale), q.z);
-      o.w = __fadd_rn(__fmul_rn(a.w, e.scale), q.w);
-      store4(e.x32 + (size_t)r * e.d + 4 * c4, o);
-      if (e.xa) store4(reinterpret_cast<TA*>(e.xa) + (size_t)r * e.d + 4 * c4, o);
-    }
+    float* x32 = e.x32 + (size_t)r * e.d;
+    TA* xa = e.xa ? reinterpret_cast<TA*>(e.xa) + (size_t)r * e.d : nullptr;
+    const float scale = e.scale;
+    row_map4<kEmbU>(e.table + (size_t)tok * e.d, e.pos + (size_t)(t + 1) * e.d, e.d >> 2, lane,
+                    [&](int c, float4 a, float4 q) {
+                      float4 o;
+                      o.x = __fadd_rn(__fmul_rn(a.x, scale), q.x);
+                      o.y = __fadd_rn(__fmul_rn(a.y, scale), q.y);
+                      o.z = __fadd_rn(__fmul_rn(a.z, scale), q.z);
+                      o.w = __fadd_rn(__fmul_rn(a.w, scale), q.w);
+                      store4(x32 + c, o);
+                      if (xa) store4(xa + c, o);
+                    });
     if constexpr (!std::is_same<TA, float>::value) {
       if (e.key.knew) step_key_row<TA>(e.key, r, tok, t + 1, lane);
     }
@@ -414,13 +463,13 @@ __global__ void __launch_bounds__(256) greedy_embed_kernel(GreedyState g, Greedy
 }
 
 cudaError_t launch_greedy_embed(const GreedyState& g, const GreedyEmbed& e, cudaStream_t s) {
-  const dim3 grid((g.rows + 7) / 8);
-  if (e.act_dtype == kF16) return launch_k(greedy_embed_kernel<__half>, grid, dim3(256), 0, s, g, e);
+  const dim3 grid((g.rows + kStepRows - 1) / kStepRows), block(32 * kStepRows);
+  if (e.act_dtype == kF16) return launch_k(greedy_embed_kernel<__half>, grid, block, 0, s, g, e);
   if (e.act_dtype == kBF16)
-    return launch_k(greedy_embed_kernel<__nv_bfloat16>, grid, dim3(256), 0, s, g, e);
+    return launch_k(greedy_embed_kernel<__nv_bfloat16>, grid, block, 0, s, g, e);
   GreedyEmbed f = e;
   f.xa = nullptr;
-  return launch_k(greedy_embed_kernel<float>, grid, dim3(256), 0, s, g, f);
+  return launch_k(greedy_embed_kernel<float>, grid, block, 0, s, g, f);
 }
 
 cudaError_t launch_greedy_update(const GreedyState& g, cudaStream_t s) {

@@ -111,6 +111,26 @@ def test_fused_vocab_argmax_lowest_id_on_ties(dt, M):
     assert (idx == ref).float().mean().item() == 1.0
 
 
+@pytest.mark.parametrize("dt", [_capi.F16, _capi.BF16])
+@pytest.mark.parametrize("M,N,K", [(3072, 32772, 512), (129, 1000, 64), (300, 4100, 448),
+                                   (1500, 9000, 576)])
+def test_fused_vocab_argmax_shapes(dt, M, N, K):
+    """The fused vocab argmax (BN = 256 tiles, N tails, K = 64..576) is the
+    argmax of the same GEMM's fp32 logits."""
+    g = torch.Generator(device="cpu").manual_seed(M + N + K)
+    A = torch.randn(M, K, generator=g).to(DEV, TDT[dt])
+    W = (torch.randn(N, K, generator=g) / K ** 0.5).to(DEV, TDT[dt])
+    bias = (torch.randn(N, generator=g) * 0.1).to(DEV)
+    keys = torch.zeros(M, dtype=torch.int64, device=DEV)
+    idx = torch.empty(M, dtype=torch.int32, device=DEV)
+    check(lib.fnmt_linear_argmax(ptr(A), K, dt, ptr(W), K, ptr(bias), M, N, K, ptr(keys),
+                                 ptr(idx), stream()), "argmax")
+    logits = linear(A, W, bias, dt)
+    torch.cuda.synchronize()
+    ref = logits.argmax(dim=1).to(torch.int32)
+    assert (idx == ref).all()
+
+
 @pytest.mark.parametrize("variant", ["l2", "l1"])
 @pytest.mark.parametrize("d", [16, 64, 512, 768])
 def test_add_norm_matches_oracle(variant, d):
